@@ -1,0 +1,166 @@
+/*
+ * pipesched_b200.h — C ABI of the B200 candidate-schedule evaluator.
+ *
+ * Drop-in boundary for the reference hot path:
+ *
+ *   ps_eval_batch      replaces  listsched.run_order            (pkg/src/pipesched/listsched.py:167-269)
+ *                      followed by schedule.makespan            (schedule.py:168-183),
+ *                      schedule.memory_trace(STRICT).peak       (schedule.py:227-237)
+ *                      and the bubble ratio                     (cli.py:115, 156),
+ *                      for a whole batch of candidate structures at once.
+ *   ps_eval_batch_host the same call on HOST buffers (copies in and out inside the call).
+ *   ps_search_round    neighbour generation + evaluation + best-of selection of one local-search
+ *                      round (no reference counterpart: SURVEY.md §0 "Not in the reference");
+ *                      its result feeds solver.start_session(warm=...) (solver.py:543-565).
+ *   ps_instance_create replaces the dict-keyed PipelineInstance tables (instance.py:62-177)
+ *                      with dense, device-resident tables.
+ *
+ * Conventions (all indices 0-based here; the Python layer converts from the reference's 1-based
+ * OpId(stage, microbatch, kind)):
+ *   op code within a stage   (j << 2) | kind,  kind F=0, B=1, W=2        (instance.py:32-59)
+ *   offload mask bit         i*m + j   (bit b lives in word b>>5, position b&31)
+ *   channel-order entry      (kind << 31) | (i << 16) | j, kind 0=OFFLOAD 1=RELOAD; 0xFFFFFFFF pads
+ *   trace entry              (rank << 30) | (i << 24) | (j << 2) | kind,
+ *                            rank 0 = compute, 1 = reload, 2 = offload   (listsched.py:230, 243)
+ *
+ * Errors never cross the ABI as exceptions: functions return PS_OK or a negative PS_ERR_* code and
+ * ps_last_error() describes the last failure on the calling thread.  Per-candidate outcomes
+ * (deadlock = the reference's OrderInfeasible, listsched.py:248-252; malformed structure) are
+ * reported in the flags array, never as call errors.
+ *
+ * Threading: an instance handle is immutable after creation and may be shared by threads and
+ * streams; every call is asynchronous on the given stream except ps_instance_create/destroy and
+ * ps_eval_batch_host.  Device pointers in the batch/result structs are owned by the caller.
+ */
+#ifndef PIPESCHED_B200_H
+#define PIPESCHED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_OK 0
+#define PS_ERR_INVALID (-1)     /* bad argument or instance invariant broken            */
+#define PS_ERR_RANGE (-2)       /* instance exceeds a supported size / value range     */
+#define PS_ERR_CUDA (-3)        /* CUDA runtime error (see ps_last_error)              */
+#define PS_ERR_NOMEM (-4)       /* device allocation failed                            */
+
+#define PS_FLAG_FEASIBLE 1u     /* complete schedule; STRICT peak <= limit by construction */
+#define PS_FLAG_DEADLOCK 2u     /* no event can start: the reference raises OrderInfeasible */
+#define PS_FLAG_MALFORMED 4u    /* stage order is not a permutation / bad channel order    */
+
+#define PS_MAX_STAGES 32
+#define PS_MAX_MICROBATCHES 4096
+
+typedef struct ps_instance ps_instance;
+
+/* Dense instance tables, host memory, copied by ps_instance_create. */
+typedef struct ps_instance_desc {
+    int32_t num_stages;            /* P, 1..PS_MAX_STAGES                                      */
+    int32_t num_microbatches;      /* m, 1..PS_MAX_MICROBATCHES                                */
+    const int64_t *proc_time;      /* [P][m][3] compute durations (F,B,W), > 0                 */
+    const int64_t *mem_delta;      /* [P][m][3] bytes; F > 0, B < 0, W < 0, sum 0             */
+    const int64_t *act_size;       /* [P][m] offloadable bytes of the F activation, 0 = none */
+    const int64_t *mem_limit;      /* [P] bytes, > 0                                           */
+    const int32_t *stage_channel;  /* [P] transfer channel of each stage (topology group)      */
+    int32_t num_channels;          /* G                                                        */
+    int64_t comm_time;             /* >= 0                                                     */
+    int64_t offload_time;          /* >= 0                                                     */
+    int32_t post_validation;       /* 1: makespan = max over stages (last W end - first F start) */
+} ps_instance_desc;
+
+/* Layout facts callers need to size candidate / result buffers. */
+typedef struct ps_instance_info {
+    int32_t num_stages;
+    int32_t num_microbatches;
+    int32_t order_stride;          /* u16 entries per stage row of stage_orders (>= 3m, mult. of 8) */
+    int32_t mask_words;            /* u32 words of one candidate's offload mask                    */
+    int32_t max_events;            /* 5*P*m: trace_stride lower bound                              */
+    int32_t value_bits;            /* 32 or 64: width of the device memory ledger                  */
+    int64_t memory_unit;           /* gcd of all byte quantities (device ledger counts in these)   */
+    int64_t busy_time;             /* sum of all proc_time (bubble numerator)                      */
+    int32_t lanes_per_candidate;   /* warp lanes that evaluate one candidate (one per stage)        */
+    int32_t device;
+} ps_instance_info;
+
+/* A batch of candidate structures, device memory. */
+typedef struct ps_cand_batch {
+    int64_t num_candidates;
+    const uint16_t *stage_orders;   /* [N][P][order_stride] op codes, each row a permutation of the
+                                       stage's 3m ops                                               */
+    const uint32_t *offload_mask;   /* [N][mask_words]                                               */
+    const uint32_t *channel_orders; /* [N][G][chan_stride] or NULL = derived (greedy) channel mode   */
+    int32_t chan_stride;
+} ps_cand_batch;
+
+/* Per-candidate outputs, device memory.  Optional arrays may be NULL. */
+typedef struct ps_result_batch {
+    int64_t *makespan;              /* [N] makespan in time quanta, -1 unless FEASIBLE             */
+    double *bubble;                 /* [N] 1 - busy/(P*makespan) in fp64, NaN unless FEASIBLE      */
+    int64_t *peak;                  /* [N][P] STRICT peak bytes per stage (optional)              */
+    uint32_t *flags;                /* [N] PS_FLAG_*                                                */
+    uint32_t *blocked;              /* [N] on DEADLOCK: bit i set = stage i still had ops (optional) */
+    uint32_t *trace_code;           /* [N][trace_stride] commit-ordered events (optional)         */
+    int32_t *trace_start;           /* [N][trace_stride] start times of those events (optional)   */
+    int32_t trace_stride;           /* >= info.max_events when trace arrays are given             */
+} ps_result_batch;
+
+/* Local-search neighbourhood: how a candidate index becomes a move. */
+typedef struct ps_move_params {
+    uint64_t seed;
+    uint32_t shift_permille;        /* share of SHIFT moves in 1/1000; the rest TOGGLE offload bits */
+    uint32_t max_shift;             /* SHIFT distance drawn from 1..max_shift, either direction      */
+} ps_move_params;
+
+typedef struct ps_search_desc {
+    const uint16_t *inc_orders;     /* device [P][order_stride]: incumbent structure              */
+    const uint32_t *inc_mask;       /* device [mask_words]                                         */
+    uint64_t round;
+    int64_t first_index;            /* global index of this shard's first neighbour               */
+    int64_t count;                  /* neighbours in this shard                                    */
+    ps_move_params moves;
+} ps_search_desc;
+
+const char *ps_version(void);
+const char *ps_last_error(void);
+
+int ps_instance_create(const ps_instance_desc *desc, int device, ps_instance **out);
+int ps_instance_destroy(ps_instance *inst);
+int ps_instance_get_info(const ps_instance *inst, ps_instance_info *out);
+
+/* Evaluate N candidates (device buffers) on `stream` (a cudaStream_t, NULL = legacy default). */
+int ps_eval_batch(const ps_instance *inst, const ps_cand_batch *batch,
+                  const ps_result_batch *results, void *stream);
+
+/* Same, with every pointer in batch/results in HOST memory (pinned for full copy speed).
+   Synchronous: returns after results are back on the host. */
+int ps_eval_batch_host(const ps_instance *inst, const ps_cand_batch *batch,
+                       const ps_result_batch *results, void *stream);
+
+/* One local-search round over neighbours [first_index, first_index+count) of the incumbent:
+   generate each move, evaluate it, and atomically fold (makespan << 32 | index) of every
+   feasible neighbour into *best_key (device int64, caller initialises it to INT64_MAX).
+   makespan_out (device int64 [count], optional) receives every neighbour's makespan or -1. */
+int ps_search_round(const ps_instance *inst, const ps_search_desc *desc,
+                    int64_t *best_key, int64_t *makespan_out, void *stream);
+
+/* Materialise neighbours [first_index, first_index+count) as full candidates (device buffers
+   shaped like ps_cand_batch: orders [count][P][order_stride], masks [count][mask_words]). */
+int ps_materialize_moves(const ps_instance *inst, const ps_search_desc *desc,
+                         uint16_t *orders_out, uint32_t *mask_out, void *stream);
+
+/* Apply neighbour `index` of round `round` to the incumbent in place (device buffers). */
+int ps_apply_move(const ps_instance *inst, uint16_t *inc_orders, uint32_t *inc_mask,
+                  const ps_move_params *moves, uint64_t round, uint64_t index, void *stream);
+
+/* INT32 issue-rate probe for the roofline denominator: runs `iters` dependent-free IADD3/LOP3
+   chains on every SM; *lane_ops receives the lane-operations executed (device int64[1]). */
+int ps_int32_probe(int64_t iters, int64_t *lane_ops, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PIPESCHED_B200_H */

@@ -1,0 +1,614 @@
+// ps_abi.cu — C ABI (include/pipesched_b200.h): instance tables, launch planning, search kernels.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/pipesched_b200.h"
+#include "ps_launch.h"
+
+using namespace ps;
+
+struct ps_instance {
+    int device;
+    int num_sms;
+    int max_smem_optin;
+    int P, m, G, L, MW, stride, mask_words;
+    int comm, toff, post, uniform, any_off;
+    int64_t busy, unit;
+    bool v64;
+    int32_t *d_proc;
+    void *d_vals;
+    void *d_limit;
+    int32_t *d_chan;
+    std::vector<uint8_t> h_offloadable;   // [P][m]
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+    return fail(PS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define PS_CUDA(call)                                            \
+    do {                                                         \
+        cudaError_t e_ = (call);                                 \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);      \
+    } while (0)
+
+// Make `dev` current for the duration of a call and restore the caller's device afterwards.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { ok = false; return; }
+        if (prev != dev && cudaSetDevice(dev) != cudaSuccess) ok = false;
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int64_t gcd64(int64_t a, int64_t b) {
+    if (a < 0) a = -a;
+    if (b < 0) b = -b;
+    while (b) {
+        int64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+struct Plan {
+    int seg, segs, K, warps;
+    bool gstate;
+    int cand_words, inc_words;
+    LaunchCfg cfg;
+    size_t scratch_bytes;
+};
+
+int words_per_candidate(const ps_instance *I, int K) {
+    int vw = I->v64 ? 2 : 1;
+    int w = I->P * K * (vw + 1) + 2 * I->P * I->m + 3 * I->P * I->MW;
+    return (w + 3) & ~3;
+}
+
+int incumbent_words(const ps_instance *I, bool moves) {
+    if (!moves) return 0;
+    int w = I->P * I->stride / 2 + I->mask_words;
+    return (w + 3) & ~3;
+}
+
+cudaError_t occupancy(int seg, bool v64, bool moves, bool gstate, int block, size_t smem, int *n) {
+    switch (seg) {
+        case 2: return eval_occupancy<2>(v64, moves, gstate, block, smem, n);
+        case 4: return eval_occupancy<4>(v64, moves, gstate, block, smem, n);
+        case 8: return eval_occupancy<8>(v64, moves, gstate, block, smem, n);
+        case 16: return eval_occupancy<16>(v64, moves, gstate, block, smem, n);
+        default: return eval_occupancy<32>(v64, moves, gstate, block, smem, n);
+    }
+}
+
+cudaError_t launch(int seg, bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c,
+                   cudaStream_t s) {
+    switch (seg) {
+        case 2: return eval_launch<2>(v64, moves, gstate, p, c, s);
+        case 4: return eval_launch<4>(v64, moves, gstate, p, c, s);
+        case 8: return eval_launch<8>(v64, moves, gstate, p, c, s);
+        case 16: return eval_launch<16>(v64, moves, gstate, p, c, s);
+        default: return eval_launch<32>(v64, moves, gstate, p, c, s);
+    }
+}
+
+// Shared-memory plan for the main pass: window K=32 (or 5m when smaller: cannot overflow),
+// as many warps per block as fit; state moves to global memory only when one warp cannot fit.
+int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
+    pl->seg = std::max(2, next_pow2(I->P));
+    pl->segs = 32 / pl->seg;
+    pl->K = std::min(32, next_pow2(5 * I->m));
+    pl->cand_words = words_per_candidate(I, pl->K);
+    pl->inc_words = incumbent_words(I, moves);
+    pl->gstate = true;
+    pl->warps = 4;
+    for (int w : {4, 2, 1}) {
+        size_t smem = (size_t)(pl->inc_words + w * pl->segs * pl->cand_words) * 4;
+        if (smem <= (size_t)I->max_smem_optin) {
+            pl->warps = w;
+            pl->gstate = false;
+            pl->cfg.smem = smem;
+            break;
+        }
+    }
+    if (pl->gstate) pl->cfg.smem = (size_t)pl->inc_words * 4;
+    if (pl->cfg.smem > (size_t)I->max_smem_optin)
+        return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
+    pl->cfg.block = 32 * pl->warps;
+    int per_sm = 0;
+    cudaError_t e = occupancy(pl->seg, I->v64, moves, pl->gstate, pl->cfg.block, pl->cfg.smem, &per_sm);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    if (per_sm < 1) per_sm = 1;
+    int64_t per_block = (int64_t)pl->warps * pl->segs;
+    int64_t want = (N + per_block - 1) / per_block;
+    pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * I->num_sms));
+    pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * per_block * pl->cand_words * 4 : 0;
+    return PS_OK;
+}
+
+// Overflow pass: window of 5m points per stage (the whole ledger), state in global memory.
+int plan_retry(const ps_instance *I, bool moves, Plan *pl) {
+    pl->seg = std::max(2, next_pow2(I->P));
+    pl->segs = 32 / pl->seg;
+    pl->K = next_pow2(5 * I->m);
+    pl->cand_words = words_per_candidate(I, pl->K);
+    pl->inc_words = incumbent_words(I, moves);
+    pl->gstate = true;
+    pl->warps = 1;
+    pl->cfg.block = 32;
+    pl->cfg.smem = (size_t)pl->inc_words * 4;
+    pl->cfg.grid = I->num_sms;
+    pl->scratch_bytes = (size_t)pl->cfg.grid * pl->segs * pl->cand_words * 4;
+    return PS_OK;
+}
+
+void fill_instance(const ps_instance *I, EvalParams *p) {
+    p->P = I->P; p->m = I->m; p->G = I->G; p->L = I->L; p->MW = I->MW; p->stride = I->stride;
+    p->comm = I->comm; p->toff = I->toff; p->post = I->post; p->uniform = I->uniform;
+    p->any_off = I->any_off; p->busy = I->busy; p->unit = I->unit;
+    p->proc = I->d_proc; p->vals = I->d_vals; p->limit = I->d_limit; p->chan = I->d_chan;
+}
+
+// Main pass + overflow pass on one stream; all scratch is stream-ordered.
+int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s) {
+    if (p.N <= 0) return PS_OK;
+    if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
+    Plan main_pl, retry_pl;
+    int rc = plan_main(I, moves, p.N, &main_pl);
+    if (rc) return rc;
+    plan_retry(I, moves, &retry_pl);
+    int32_t *ovf = nullptr;
+    uint32_t *scratch = nullptr, *scratch2 = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&ovf, (size_t)(p.N + 1) * sizeof(int32_t), s));
+    PS_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s));
+    if (main_pl.scratch_bytes) PS_CUDA(cudaMallocAsync((void **)&scratch, main_pl.scratch_bytes, s));
+    PS_CUDA(cudaMallocAsync((void **)&scratch2, retry_pl.scratch_bytes, s));
+
+    p.ovf_count = ovf;
+    p.ovf_list = ovf + 1;
+    p.work_list = nullptr;
+    p.work_count = nullptr;
+    p.K = main_pl.K;
+    p.cand_words = main_pl.cand_words;
+    p.inc_words = main_pl.inc_words;
+    p.gstate = scratch;
+    cudaError_t e = launch(main_pl.seg, I->v64, moves, main_pl.gstate, p, main_pl.cfg, s);
+    if (e != cudaSuccess) return cuda_fail(e, "evaluator launch");
+
+    EvalParams q = p;
+    q.work_list = ovf + 1;
+    q.work_count = ovf;
+    q.ovf_list = nullptr;     // the full-ledger window cannot overflow
+    q.ovf_count = nullptr;
+    q.K = retry_pl.K;
+    q.cand_words = retry_pl.cand_words;
+    q.inc_words = retry_pl.inc_words;
+    q.gstate = scratch2;
+    e = launch(retry_pl.seg, I->v64, moves, true, q, retry_pl.cfg, s);
+    if (e != cudaSuccess) return cuda_fail(e, "evaluator overflow launch");
+    if (scratch) PS_CUDA(cudaFreeAsync(scratch, s));
+    PS_CUDA(cudaFreeAsync(scratch2, s));
+    PS_CUDA(cudaFreeAsync(ovf, s));
+    return PS_OK;
+}
+
+// ---- search helpers ------------------------------------------------------------------------
+
+struct MoveCtx {
+    int P, m, L, stride, mask_words, uniform, any_off;
+    const void *vals;
+    bool v64;
+};
+
+__device__ bool ctx_offloadable(const MoveCtx &c, int s, int j) {
+    int idx = (c.uniform ? s : s * c.m + j) * 4 + 3;
+    if (c.v64) return reinterpret_cast<const long long *>(c.vals)[idx] > 0;
+    return reinterpret_cast<const int *>(c.vals)[idx] > 0;
+}
+
+__device__ Move ctx_decode(const MoveCtx &c, const ps_move_params &mp, uint64_t round, uint64_t index) {
+    return decode_move(mp.seed, round, index, c.P, c.m, mp.shift_permille, mp.max_shift,
+                       c.any_off != 0, [&](int s, int j) { return ctx_offloadable(c, s, j); });
+}
+
+// One warp per (neighbour, stage) row.
+__global__ void materialize_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first,
+                                   int64_t count, const uint16_t *inc, const uint32_t *inc_mask,
+                                   uint16_t *out, uint32_t *out_mask) {
+    int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (row >= count * c.P) return;
+    int64_t n = row / c.P;
+    int s = (int)(row % c.P);
+    Move mv = ctx_decode(c, mp, round, (uint64_t)(first + n));
+    const uint16_t *src = inc + (size_t)s * c.stride;
+    uint16_t *dst = out + ((size_t)n * c.P + s) * c.stride;
+    bool shift = mv.type == MOVE_SHIFT && mv.stage == s;
+    for (int q = lane; q < c.stride; q += 32)
+        dst[q] = q < c.L ? src[shift ? shifted_position(q, mv.a, mv.b) : q] : (uint16_t)0;
+    if (s == 0)
+        for (int w = lane; w < c.mask_words; w += 32) {
+            uint32_t v = inc_mask[w];
+            if (mv.type == MOVE_TOGGLE) {
+                int b = mv.stage * c.m + mv.mb;
+                if ((b >> 5) == w) v ^= 1u << (b & 31);
+            }
+            out_mask[(size_t)n * c.mask_words + w] = v;
+        }
+}
+
+__global__ void apply_move_kernel(MoveCtx c, ps_move_params mp, uint64_t round, uint64_t index,
+                                  uint16_t *inc, uint32_t *inc_mask) {
+    if (threadIdx.x) return;
+    Move mv = ctx_decode(c, mp, round, index);
+    if (mv.type == MOVE_SHIFT) {
+        uint16_t *row = inc + (size_t)mv.stage * c.stride;
+        uint16_t v = row[mv.a];
+        if (mv.a < mv.b)
+            for (int q = mv.a; q < mv.b; ++q) row[q] = row[q + 1];
+        else
+            for (int q = mv.a; q > mv.b; --q) row[q] = row[q - 1];
+        row[mv.b] = v;
+    } else if (mv.type == MOVE_TOGGLE) {
+        int b = mv.stage * c.m + mv.mb;
+        inc_mask[b >> 5] ^= 1u << (b & 31);
+    }
+}
+
+// Independent IADD3/LOP3/IMAD chains: the INT32 issue ceiling of the roofline.
+__global__ void int32_probe_kernel(int64_t iters, uint32_t seed, unsigned long long *lane_ops, uint32_t *sink) {
+    uint32_t a0 = threadIdx.x ^ seed, a1 = a0 * 3u, a2 = a0 + 7u, a3 = a0 ^ 0x55u;
+    uint32_t b0 = a0 + 1u, b1 = a1 + 2u, b2 = a2 + 3u, b3 = a3 + 4u;
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 = (a0 + b1) ^ b2; a1 = (a1 + b2) ^ b3; a2 = (a2 + b3) ^ b0; a3 = (a3 + b0) ^ b1;
+            b0 = b0 * 0x9E37u + a1; b1 = b1 * 0x85EBu + a2; b2 = b2 * 0xC2B2u + a3; b3 = b3 * 0x27D4u + a0;
+        }
+    }
+    uint32_t r = a0 ^ a1 ^ a2 ^ a3 ^ b0 ^ b1 ^ b2 ^ b3;
+    if (r == seed) sink[0] = r;   // keeps the chains alive
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        atomicAdd(lane_ops, (unsigned long long)iters * 8ull * 12ull * blockDim.x * gridDim.x);
+}
+
+MoveCtx move_ctx(const ps_instance *I) {
+    MoveCtx c;
+    c.P = I->P; c.m = I->m; c.L = I->L; c.stride = I->stride; c.mask_words = I->mask_words;
+    c.uniform = I->uniform; c.any_off = I->any_off; c.vals = I->d_vals; c.v64 = I->v64;
+    return c;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+const char *ps_version(void) { return "pipesched_b200 0.1.0 (sm_100a)"; }
+
+const char *ps_last_error(void) { return g_last_error.c_str(); }
+
+int ps_instance_create(const ps_instance_desc *d, int device, ps_instance **out) {
+    if (!d || !out) return fail(PS_ERR_INVALID, "null argument");
+    *out = nullptr;
+    const int P = d->num_stages, m = d->num_microbatches;
+    if (P < 1 || P > PS_MAX_STAGES) return fail(PS_ERR_RANGE, "num_stages %d outside 1..%d", P, PS_MAX_STAGES);
+    if (m < 1 || m > PS_MAX_MICROBATCHES)
+        return fail(PS_ERR_RANGE, "num_microbatches %d outside 1..%d", m, PS_MAX_MICROBATCHES);
+    if (!d->proc_time || !d->mem_delta || !d->act_size || !d->mem_limit || !d->stage_channel)
+        return fail(PS_ERR_INVALID, "null table");
+    if (d->comm_time < 0 || d->offload_time < 0) return fail(PS_ERR_INVALID, "comm_time and offload_time must be >= 0");
+    if (d->num_channels < 1 || d->num_channels > P) return fail(PS_ERR_INVALID, "num_channels %d", d->num_channels);
+    // instance invariants (reference instance.py:88-126)
+    int64_t unit = 0, busy = 0, n_off = 0;
+    bool uniform = true, any_off = false;
+    for (int i = 0; i < P; ++i) {
+        if (d->mem_limit[i] <= 0) return fail(PS_ERR_INVALID, "mem_limit must be positive for stage %d", i + 1);
+        if (d->stage_channel[i] < 0 || d->stage_channel[i] >= d->num_channels)
+            return fail(PS_ERR_INVALID, "stage %d has channel %d", i + 1, d->stage_channel[i]);
+        unit = gcd64(unit, d->mem_limit[i]);
+        for (int j = 0; j < m; ++j) {
+            const int64_t *t = d->proc_time + ((size_t)i * m + j) * 3;
+            const int64_t *v = d->mem_delta + ((size_t)i * m + j) * 3;
+            int64_t g = d->act_size[(size_t)i * m + j];
+            for (int k = 0; k < 3; ++k) {
+                if (t[k] <= 0) return fail(PS_ERR_INVALID, "proc_time must be positive at (%d,%d,%d)", i + 1, j + 1, k);
+                busy += t[k];
+                unit = gcd64(unit, v[k]);
+            }
+            if (v[0] + v[1] + v[2] != 0) return fail(PS_ERR_INVALID, "mem_delta sum nonzero for stage %d microbatch %d", i + 1, j + 1);
+            if (!(v[0] > 0 && v[1] < 0 && v[2] < 0))
+                return fail(PS_ERR_INVALID, "mem_delta signs wrong for stage %d microbatch %d", i + 1, j + 1);
+            if (g < 0 || g > v[0]) return fail(PS_ERR_INVALID, "act_size outside [0, mem_delta_F] at stage %d microbatch %d", i + 1, j + 1);
+            if (g > 0) { unit = gcd64(unit, g); any_off = true; ++n_off; }
+            if (j > 0) {
+                const int64_t *t0 = d->proc_time + (size_t)i * m * 3;
+                const int64_t *v0 = d->mem_delta + (size_t)i * m * 3;
+                for (int k = 0; k < 3; ++k)
+                    if (t[k] != t0[k] || v[k] != v0[k]) uniform = false;
+                if (g != d->act_size[(size_t)i * m]) uniform = false;
+            }
+        }
+    }
+    // every event time must stay below 2^29 (times are packed as (t << 2 | state) in 32 bits)
+    double horizon = (double)busy + 2.0 * n_off * d->offload_time + (2.0 * m * P + 1.0) * d->comm_time;
+    if (horizon >= (double)(1 << 29))
+        return fail(PS_ERR_RANGE, "instance horizon %.0f quanta exceeds the 2^29 time range", horizon);
+    // ledger width: usage never exceeds the sum of a stage's F deltas
+    bool v64 = false;
+    for (int i = 0; i < P; ++i) {
+        int64_t s = d->mem_limit[i] / unit;
+        for (int j = 0; j < m; ++j) s += d->mem_delta[((size_t)i * m + j) * 3] / unit;
+        if (s > (int64_t)(INT32_MAX / 4)) v64 = true;
+    }
+
+    ps_instance *I = new (std::nothrow) ps_instance();
+    if (!I) return fail(PS_ERR_NOMEM, "host allocation");
+    I->device = device;
+    I->P = P; I->m = m; I->G = d->num_channels; I->L = 3 * m; I->MW = (m + 31) / 32;
+    I->stride = (3 * m + 7) & ~7;
+    I->mask_words = (P * m + 31) / 32;
+    I->comm = (int)d->comm_time; I->toff = (int)d->offload_time; I->post = d->post_validation != 0;
+    I->uniform = uniform; I->any_off = any_off; I->busy = busy; I->unit = unit; I->v64 = v64;
+    I->h_offloadable.resize((size_t)P * m);
+    for (size_t k = 0; k < (size_t)P * m; ++k) I->h_offloadable[k] = d->act_size[k] > 0;
+
+    DeviceGuard guard(device);
+    if (!guard.ok) { delete I; return fail(PS_ERR_CUDA, "cannot select device %d", device); }
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) { delete I; return cuda_fail(e, "cudaGetDeviceProperties"); }
+    I->num_sms = prop.multiProcessorCount;
+    I->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+
+    const int rows = uniform ? P : P * m;
+    std::vector<int32_t> proc((size_t)rows * 3), chan(P);
+    std::vector<int64_t> vals64((size_t)rows * 4), lim64(P);
+    for (int r = 0; r < rows; ++r) {
+        size_t src = uniform ? (size_t)r * m : (size_t)r;   // uniform: row r = stage r, microbatch 0
+        for (int k = 0; k < 3; ++k) {
+            proc[(size_t)r * 3 + k] = (int32_t)d->proc_time[src * 3 + k];
+            vals64[(size_t)r * 4 + k] = d->mem_delta[src * 3 + k] / unit;
+        }
+        vals64[(size_t)r * 4 + 3] = d->act_size[src] / unit;
+    }
+    for (int i = 0; i < P; ++i) {
+        lim64[i] = d->mem_limit[i] / unit;
+        chan[i] = d->stage_channel[i];
+    }
+    size_t vb = v64 ? 8 : 4;
+    e = cudaMalloc((void **)&I->d_proc, proc.size() * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&I->d_vals, vals64.size() * vb);
+    if (e == cudaSuccess) e = cudaMalloc(&I->d_limit, (size_t)P * vb);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&I->d_chan, (size_t)P * 4);
+    if (e != cudaSuccess) { ps_instance_destroy(I); return fail(PS_ERR_NOMEM, "device tables: %s", cudaGetErrorString(e)); }
+    std::vector<int32_t> vals32, lim32;
+    const void *vsrc = vals64.data(), *lsrc = lim64.data();
+    if (!v64) {
+        vals32.assign(vals64.begin(), vals64.end());
+        lim32.assign(lim64.begin(), lim64.end());
+        vsrc = vals32.data();
+        lsrc = lim32.data();
+    }
+    e = cudaMemcpy(I->d_proc, proc.data(), proc.size() * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(I->d_vals, vsrc, vals64.size() * vb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(I->d_limit, lsrc, (size_t)P * vb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(I->d_chan, chan.data(), (size_t)P * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { ps_instance_destroy(I); return cuda_fail(e, "upload instance tables"); }
+    *out = I;
+    return PS_OK;
+}
+
+int ps_instance_destroy(ps_instance *I) {
+    if (!I) return PS_OK;
+    DeviceGuard guard(I->device);
+    cudaFree(I->d_proc);
+    cudaFree(I->d_vals);
+    cudaFree(I->d_limit);
+    cudaFree(I->d_chan);
+    delete I;
+    return PS_OK;
+}
+
+int ps_instance_get_info(const ps_instance *I, ps_instance_info *o) {
+    if (!I || !o) return fail(PS_ERR_INVALID, "null argument");
+    o->num_stages = I->P;
+    o->num_microbatches = I->m;
+    o->order_stride = I->stride;
+    o->mask_words = I->mask_words;
+    o->max_events = 5 * I->P * I->m;
+    o->value_bits = I->v64 ? 64 : 32;
+    o->memory_unit = I->unit;
+    o->busy_time = I->busy;
+    o->lanes_per_candidate = std::max(2, next_pow2(I->P));
+    o->device = I->device;
+    return PS_OK;
+}
+
+int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
+    if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
+    if (b->num_candidates < 0) return fail(PS_ERR_INVALID, "negative candidate count");
+    if (b->num_candidates == 0) return PS_OK;
+    if (!b->stage_orders || !b->offload_mask) return fail(PS_ERR_INVALID, "stage_orders and offload_mask are required");
+    if (!r->makespan || !r->flags || !r->bubble) return fail(PS_ERR_INVALID, "makespan, bubble and flags outputs are required");
+    if (b->channel_orders && b->chan_stride < 1) return fail(PS_ERR_INVALID, "chan_stride must be positive");
+    if ((r->trace_code != nullptr) != (r->trace_start != nullptr))
+        return fail(PS_ERR_INVALID, "trace_code and trace_start go together");
+    if (r->trace_code && r->trace_stride < 5 * I->P * I->m)
+        return fail(PS_ERR_INVALID, "trace_stride %d < 5*P*m", r->trace_stride);
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    EvalParams p;
+    memset(&p, 0, sizeof p);
+    fill_instance(I, &p);
+    p.N = b->num_candidates;
+    p.orders = b->stage_orders;
+    p.masks = b->offload_mask;
+    p.chorders = b->channel_orders;
+    p.chan_stride = b->chan_stride;
+    p.makespan = r->makespan;
+    p.bubble = r->bubble;
+    p.peak = r->peak;
+    p.flags = r->flags;
+    p.blocked = r->blocked;
+    p.tcode = r->trace_code;
+    p.tstart = r->trace_start;
+    p.tstride = r->trace_stride;
+    return run_eval(I, p, false, (cudaStream_t)stream);
+}
+
+int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
+    if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
+    const int64_t N = b->num_candidates;
+    if (N <= 0) return N == 0 ? PS_OK : fail(PS_ERR_INVALID, "negative candidate count");
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n_ord = (size_t)N * I->P * I->stride * 2, n_mask = (size_t)N * I->mask_words * 4;
+    const size_t n_chan = b->channel_orders ? (size_t)N * I->G * b->chan_stride * 4 : 0;
+    const size_t n_peak = r->peak ? (size_t)N * I->P * 8 : 0;
+    const size_t n_tr = r->trace_code ? (size_t)N * r->trace_stride * 4 : 0;
+    const size_t n_blk = r->blocked ? (size_t)N * 4 : 0;
+    // one device arena: inputs, then outputs
+    size_t off[10], total = 0;
+    size_t sizes[10] = {n_ord, n_mask, n_chan, (size_t)N * 8, (size_t)N * 8, n_peak, (size_t)N * 4, n_blk, n_tr, n_tr};
+    for (int k = 0; k < 10; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
+    char *arena = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
+    PS_CUDA(cudaMemcpyAsync(arena + off[0], b->stage_orders, n_ord, cudaMemcpyHostToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(arena + off[1], b->offload_mask, n_mask, cudaMemcpyHostToDevice, s));
+    if (n_chan) PS_CUDA(cudaMemcpyAsync(arena + off[2], b->channel_orders, n_chan, cudaMemcpyHostToDevice, s));
+    ps_cand_batch db = *b;
+    db.stage_orders = (const uint16_t *)(arena + off[0]);
+    db.offload_mask = (const uint32_t *)(arena + off[1]);
+    db.channel_orders = n_chan ? (const uint32_t *)(arena + off[2]) : nullptr;
+    ps_result_batch dr = *r;
+    dr.makespan = (int64_t *)(arena + off[3]);
+    dr.bubble = (double *)(arena + off[4]);
+    dr.peak = n_peak ? (int64_t *)(arena + off[5]) : nullptr;
+    dr.flags = (uint32_t *)(arena + off[6]);
+    dr.blocked = n_blk ? (uint32_t *)(arena + off[7]) : nullptr;
+    dr.trace_code = n_tr ? (uint32_t *)(arena + off[8]) : nullptr;
+    dr.trace_start = n_tr ? (int32_t *)(arena + off[9]) : nullptr;
+    int rc = ps_eval_batch(I, &db, &dr, stream);
+    if (rc) { cudaFreeAsync(arena, s); return rc; }
+    PS_CUDA(cudaMemcpyAsync(r->makespan, dr.makespan, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaMemcpyAsync(r->bubble, dr.bubble, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaMemcpyAsync(r->flags, dr.flags, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
+    if (n_peak) PS_CUDA(cudaMemcpyAsync(r->peak, dr.peak, n_peak, cudaMemcpyDeviceToHost, s));
+    if (n_blk) PS_CUDA(cudaMemcpyAsync(r->blocked, dr.blocked, n_blk, cudaMemcpyDeviceToHost, s));
+    if (n_tr) {
+        PS_CUDA(cudaMemcpyAsync(r->trace_code, dr.trace_code, n_tr, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(r->trace_start, dr.trace_start, n_tr, cudaMemcpyDeviceToHost, s));
+    }
+    PS_CUDA(cudaFreeAsync(arena, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    return PS_OK;
+}
+
+int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
+                    void *stream) {
+    if (!I || !d || !best_key) return fail(PS_ERR_INVALID, "null argument");
+    if (!d->inc_orders || !d->inc_mask) return fail(PS_ERR_INVALID, "incumbent buffers are required");
+    if (d->count < 0 || d->first_index < 0) return fail(PS_ERR_INVALID, "negative shard range");
+    if ((uint64_t)(d->first_index + d->count) > 0xFFFFFFFFull)
+        return fail(PS_ERR_RANGE, "neighbour indices must stay below 2^32");
+    if (d->moves.shift_permille > 1000u || d->moves.max_shift < 1u)
+        return fail(PS_ERR_INVALID, "shift_permille must be <= 1000 and max_shift >= 1");
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    EvalParams p;
+    memset(&p, 0, sizeof p);
+    fill_instance(I, &p);
+    p.N = d->count;
+    p.inc_orders = d->inc_orders;
+    p.inc_mask = d->inc_mask;
+    p.seed = d->moves.seed;
+    p.round = d->round;
+    p.first_index = d->first_index;
+    p.shift_permille = d->moves.shift_permille;
+    p.max_shift = d->moves.max_shift;
+    p.makespan = makespan_out;
+    p.best_key = (long long *)best_key;
+    return run_eval(I, p, true, (cudaStream_t)stream);
+}
+
+int ps_materialize_moves(const ps_instance *I, const ps_search_desc *d, uint16_t *orders_out, uint32_t *mask_out,
+                         void *stream) {
+    if (!I || !d || !orders_out || !mask_out) return fail(PS_ERR_INVALID, "null argument");
+    if (d->count <= 0) return PS_OK;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    int64_t warps = d->count * I->P;
+    int64_t blocks = (warps * 32 + 255) / 256;
+    materialize_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+        move_ctx(I), d->moves, d->round, d->first_index, d->count, d->inc_orders, d->inc_mask, orders_out, mask_out);
+    PS_CUDA(cudaGetLastError());
+    return PS_OK;
+}
+
+int ps_apply_move(const ps_instance *I, uint16_t *inc_orders, uint32_t *inc_mask, const ps_move_params *mp,
+                  uint64_t round, uint64_t index, void *stream) {
+    if (!I || !inc_orders || !inc_mask || !mp) return fail(PS_ERR_INVALID, "null argument");
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    apply_move_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(move_ctx(I), *mp, round, index, inc_orders, inc_mask);
+    PS_CUDA(cudaGetLastError());
+    return PS_OK;
+}
+
+int ps_int32_probe(int64_t iters, int64_t *lane_ops, void *stream) {
+    if (!lane_ops || iters < 1) return fail(PS_ERR_INVALID, "bad probe arguments");
+    int dev, sms;
+    PS_CUDA(cudaGetDevice(&dev));
+    PS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    uint32_t *sink = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    PS_CUDA(cudaMallocAsync((void **)&sink, 4, s));
+    int32_probe_kernel<<<sms * 8, 256, 0, s>>>(iters, 0x1234567u, (unsigned long long *)lane_ops, sink);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA(cudaFreeAsync(sink, s));
+    return PS_OK;
+}
+
+}  // extern "C"

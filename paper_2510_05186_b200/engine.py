@@ -1,0 +1,151 @@
+"""Batched candidate evaluation on the GPU (the hot path behind ``run_order``).
+
+``DeviceInstance`` owns one ``ps_instance`` handle (dense tables resident in
+HBM); ``evaluate`` / ``evaluate_host`` run ``ps_eval_batch`` /
+``ps_eval_batch_host`` over a batch of candidate structures and return
+makespan, fp64 bubble ratio, per-stage STRICT peaks, feasibility flags, the
+blocked-stage mask of deadlocked candidates and optionally the commit-ordered
+event trace.  PyTorch provides device memory and the stream; the kernels are
+the hand-written sm_100a code in ``csrc/``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .packing import PackedInstance, pack_instance
+
+
+@dataclass
+class EvalResult:
+    makespan: object       # int64 [N]; -1 unless feasible
+    bubble: object         # float64 [N]
+    flags: object          # int32 [N] (PS_FLAG_* bits)
+    peak: object = None    # int64 [N, P]
+    blocked: object = None  # int32 [N]
+    trace_code: object = None   # int32 [N, E]
+    trace_start: object = None  # int32 [N, E]
+
+    def feasible(self):
+        return (self.flags & N.FLAG_FEASIBLE) != 0
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+class DeviceInstance:
+    """A PipelineInstance's tables on one CUDA device."""
+
+    def __init__(self, inst, device: int | None = None, packed: PackedInstance | None = None):
+        import torch
+        N.require_cuda()
+        self.lib = N.load_library()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.packed = packed if packed is not None else pack_instance(inst)
+        pk = self.packed
+        self._keep = [np.ascontiguousarray(a) for a in
+                      (pk.proc_time, pk.mem_delta, pk.act_size, pk.mem_limit, pk.stage_channel)]
+        desc = N.InstanceDesc(pk.num_stages, pk.num_microbatches,
+                              *[a.ctypes.data for a in self._keep],
+                              pk.num_channels, pk.comm_time, pk.offload_time, int(pk.post_validation))
+        h = C.c_void_p()
+        N.check(self.lib.ps_instance_create(C.byref(desc), self.device, C.byref(h)))
+        self.handle = h
+        info = N.InstanceInfo()
+        N.check(self.lib.ps_instance_get_info(h, C.byref(info)))
+        self.info = info
+        self._finalizer = weakref.finalize(self, self.lib.ps_instance_destroy, h)
+
+    @property
+    def P(self):
+        return self.packed.num_stages
+
+    @property
+    def m(self):
+        return self.packed.num_microbatches
+
+    def _stream(self, stream):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return C.c_void_p(stream.cuda_stream)
+
+    def alloc_results(self, n: int, peak=True, trace=False, blocked=True):
+        import torch
+        dev = torch.device("cuda", self.device)
+        E = self.info.max_events
+        return EvalResult(
+            makespan=torch.empty(n, dtype=torch.int64, device=dev),
+            bubble=torch.empty(n, dtype=torch.float64, device=dev),
+            flags=torch.empty(n, dtype=torch.int32, device=dev),
+            peak=torch.empty((n, self.P), dtype=torch.int64, device=dev) if peak else None,
+            blocked=torch.empty(n, dtype=torch.int32, device=dev) if blocked else None,
+            trace_code=torch.empty((n, E), dtype=torch.int32, device=dev) if trace else None,
+            trace_start=torch.empty((n, E), dtype=torch.int32, device=dev) if trace else None)
+
+    def _batch_structs(self, n, orders, masks, chans, res: EvalResult):
+        cb = N.CandBatch(n, _ptr(orders), _ptr(masks), _ptr(chans),
+                         int(chans.shape[-1]) if chans is not None else 0)
+        rb = N.ResultBatch(_ptr(res.makespan), _ptr(res.bubble), _ptr(res.peak), _ptr(res.flags),
+                           _ptr(res.blocked), _ptr(res.trace_code), _ptr(res.trace_start),
+                           int(res.trace_code.shape[-1]) if res.trace_code is not None else 0)
+        return cb, rb
+
+    def evaluate(self, orders, masks, chans=None, out: EvalResult | None = None, peak=True,
+                 trace=False, stream=None) -> EvalResult:
+        """Device tensors in, device tensors out; asynchronous on `stream`."""
+        n = int(orders.shape[0])
+        res = out if out is not None else self.alloc_results(n, peak=peak, trace=trace)
+        cb, rb = self._batch_structs(n, orders, masks, chans, res)
+        N.check(self.lib.ps_eval_batch(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
+        return res
+
+    def evaluate_host(self, orders: np.ndarray, masks: np.ndarray, chans=None, peak=True,
+                      trace=False, out: EvalResult | None = None, stream=None) -> EvalResult:
+        """Host (ideally pinned) numpy buffers in and out: copies inside the call."""
+        n = int(orders.shape[0])
+        if out is None:
+            E = self.info.max_events
+            out = EvalResult(np.empty(n, np.int64), np.empty(n, np.float64), np.empty(n, np.int32),
+                             np.empty((n, self.P), np.int64) if peak else None, np.empty(n, np.int32),
+                             np.empty((n, E), np.int32) if trace else None,
+                             np.empty((n, E), np.int32) if trace else None)
+        cb, rb = self._batch_structs(n, np.ascontiguousarray(orders), np.ascontiguousarray(masks),
+                                     None if chans is None else np.ascontiguousarray(chans), out)
+        N.check(self.lib.ps_eval_batch_host(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
+        return out
+
+
+_CACHE: dict = {}
+_CACHE_LOCK = threading.Lock()
+
+
+def device_instance(inst, device: int | None = None) -> DeviceInstance:
+    """Cached DeviceInstance per (instance object, device)."""
+    import torch
+    N.require_cuda()
+    dev = torch.cuda.current_device() if device is None else int(device)
+    key = (id(inst), dev)
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None and hit[0]() is inst:
+            return hit[1]
+    di = DeviceInstance(inst, dev)
+    try:
+        ref = weakref.ref(inst, lambda _r, k=key: _CACHE.pop(k, None))
+    except TypeError:
+        return di
+    with _CACHE_LOCK:
+        _CACHE[key] = (ref, di)
+    return di

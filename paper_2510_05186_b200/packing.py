@@ -1,0 +1,171 @@
+"""Dense encodings shared by the host API, the C ABI and the oracle.
+
+Instance tables (``pack_instance``) follow ``ps_instance_desc``; candidates
+(``encode_candidates``) follow ``ps_cand_batch``:
+
+* stage order row i: u16 op codes ``(j-1) << 2 | kind`` padded to
+  ``order_stride`` (a multiple of 8, >= 3m);
+* offload mask: bit ``(i-1)*m + (j-1)`` of ``ceil(P*m/32)`` u32 words;
+* explicit channel orders: u32 ``kind << 31 | (i-1) << 16 | (j-1)``
+  (kind 1 = reload), padded with 0xFFFFFFFF.
+
+Stage/microbatch indices are 1-based in ``OpId`` exactly as in the reference
+(instance.py:51-59); every encoding here is 0-based.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .instance import OpId, OpKind
+
+PAD_CHANNEL = 0xFFFFFFFF
+
+
+@dataclass(frozen=True)
+class PackedInstance:
+    num_stages: int
+    num_microbatches: int
+    proc_time: np.ndarray      # int64 [P, m, 3]
+    mem_delta: np.ndarray      # int64 [P, m, 3]
+    act_size: np.ndarray       # int64 [P, m]
+    mem_limit: np.ndarray      # int64 [P]
+    stage_channel: np.ndarray  # int32 [P]
+    num_channels: int
+    comm_time: int
+    offload_time: int
+    post_validation: bool
+
+    @property
+    def order_stride(self) -> int:
+        return (3 * self.num_microbatches + 7) & ~7
+
+    @property
+    def mask_words(self) -> int:
+        return (self.num_stages * self.num_microbatches + 31) // 32
+
+    @property
+    def busy_time(self) -> int:
+        return int(self.proc_time.sum())
+
+
+def pack_instance(inst) -> PackedInstance:
+    """Dense tables of a PipelineInstance (ours or the reference's: duck-typed)."""
+    P, m = inst.num_stages, inst.num_microbatches
+    proc = np.empty((P, m, 3), np.int64)
+    delta = np.empty((P, m, 3), np.int64)
+    act = np.zeros((P, m), np.int64)
+    for i in range(1, P + 1):
+        for j in range(1, m + 1):
+            for k in range(3):
+                op = OpId(i, j, OpKind(k))
+                proc[i - 1, j - 1, k] = inst.proc_time[op]
+                delta[i - 1, j - 1, k] = inst.mem_delta[op]
+            act[i - 1, j - 1] = inst.act_size.get(OpId(i, j, OpKind.F), 0)
+    limit = np.array([inst.mem_limit[i] for i in range(1, P + 1)], np.int64)
+    chan = np.array([inst.stage_channel(i) for i in range(1, P + 1)], np.int32)
+    return PackedInstance(P, m, proc, delta, act, limit, chan, len(inst.topology_groups),
+                          int(inst.comm_time), int(inst.offload_time), bool(inst.post_validation))
+
+
+def op_code(op) -> int:
+    return ((op[1] - 1) << 2) | int(op[2])
+
+
+def decode_op(stage0: int, code: int) -> OpId:
+    return OpId(stage0 + 1, (code >> 2) + 1, OpKind(code & 3))
+
+
+def _kind_is_reload(kind) -> bool:
+    return getattr(kind, "value", kind) == "reload"
+
+
+def encode_candidate(pk: PackedInstance, stage_orders, offloaded, channel_orders=None,
+                     orders_out=None, mask_out=None, chan_out=None):
+    """One candidate into preallocated rows (or fresh arrays).  Raises
+    ValueError for structurally malformed input and KeyError (as the
+    reference does at listsched.py:157/201) for offloading an op that has no
+    offloadable activation."""
+    P, m = pk.num_stages, pk.num_microbatches
+    if orders_out is None:
+        orders_out = np.zeros((P, pk.order_stride), np.uint16)
+    if mask_out is None:
+        mask_out = np.zeros(pk.mask_words, np.uint32)
+    for i in range(1, P + 1):
+        try:
+            row = stage_orders[i]
+        except KeyError:
+            raise KeyError(i) from None
+        if len(row) != 3 * m:
+            raise ValueError(f"stage {i} order has {len(row)} ops, expected {3 * m}")
+        codes = np.fromiter(((op[1] - 1) << 2 | int(op[2]) for op in row), np.int64, 3 * m)
+        stages = np.fromiter((op[0] for op in row), np.int64, 3 * m)
+        mbs = codes >> 2
+        if (stages != i).any() or (mbs < 0).any() or (mbs >= m).any():
+            raise ValueError(f"stage {i} order holds ops of another stage or microbatch range")
+        if len(np.unique(codes)) != 3 * m:
+            raise ValueError(f"stage {i} order is not a permutation of its ops")
+        orders_out[i - 1, :3 * m] = codes
+    mask_out[:] = 0
+    for op in offloaded:
+        i, j, k = op
+        if int(k) != 0 or not (1 <= i <= P and 1 <= j <= m) or pk.act_size[i - 1, j - 1] <= 0:
+            raise KeyError(op)
+        b = (i - 1) * m + (j - 1)
+        mask_out[b >> 5] |= np.uint32(1 << (b & 31))
+    if channel_orders is not None:
+        width = chan_out.shape[1] if chan_out is not None else max(
+            [len(v) for v in channel_orders.values()] + [1])
+        if chan_out is None:
+            chan_out = np.full((pk.num_channels, width), PAD_CHANNEL, np.uint32)
+        chan_out[:] = PAD_CHANNEL
+        off = set(tuple(x) for x in offloaded)
+        for g in range(pk.num_channels):
+            seq = channel_orders.get(g, ())
+            if len(seq) > width:
+                raise ValueError(f"channel {g} order longer than chan_stride {width}")
+            seen = set()
+            for q, (op, kind) in enumerate(seq):
+                i, j, k = op
+                if tuple(op) not in off:
+                    raise KeyError(op)
+                if pk.stage_channel[i - 1] != g:
+                    raise ValueError(f"{op} is not served by channel {g}")
+                rel = _kind_is_reload(kind)
+                if (tuple(op), rel) in seen:
+                    raise ValueError(f"duplicate transfer {op} on channel {g}")
+                seen.add((tuple(op), rel))
+                chan_out[g, q] = (int(rel) << 31) | ((i - 1) << 16) | (j - 1)
+    return orders_out, mask_out, chan_out
+
+
+def encode_candidates(pk: PackedInstance, candidates, explicit: bool = False):
+    """List of (stage_orders, offloaded[, channel_orders]) -> dense numpy batch."""
+    n = len(candidates)
+    orders = np.zeros((n, pk.num_stages, pk.order_stride), np.uint16)
+    masks = np.zeros((n, pk.mask_words), np.uint32)
+    chans = None
+    if explicit:
+        width = max([len(seq) for c in candidates for seq in c[2].values()] + [1])
+        chans = np.full((n, pk.num_channels, width), PAD_CHANNEL, np.uint32)
+    for c, cand in enumerate(candidates):
+        encode_candidate(pk, cand[0], cand[1], cand[2] if explicit else None, orders[c], masks[c],
+                         chans[c] if explicit else None)
+    return orders, masks, chans
+
+
+def decode_orders(pk: PackedInstance, orders_row: np.ndarray) -> dict:
+    """[P, stride] op codes -> {stage: tuple(OpId)}."""
+    L = 3 * pk.num_microbatches
+    return {i + 1: tuple(decode_op(i, int(c)) for c in orders_row[i, :L]) for i in range(pk.num_stages)}
+
+
+def decode_mask(pk: PackedInstance, mask_row: np.ndarray) -> frozenset:
+    m = pk.num_microbatches
+    out = []
+    for b in range(pk.num_stages * m):
+        if (int(mask_row[b >> 5]) >> (b & 31)) & 1:
+            out.append(OpId(b // m + 1, b % m + 1, OpKind.F))
+    return frozenset(out)

@@ -1,0 +1,190 @@
+"""GPU local search over candidate structures.
+
+One round evaluates ``neighbours`` moves of the incumbent — each decoded on the
+device from Philox4x32-10 keyed by (seed, round, global index), DESIGN.md §4
+— with the evaluator kernel, folds ``(makespan << 32 | index)`` of every
+feasible neighbour into one int64 key with an atomic min, combines the key
+across ranks with one NCCL all-reduce(MIN) of 8 bytes, and applies the winning
+move in place on every rank when it strictly improves the incumbent.  The
+candidate set of a round is identical at 1/2/4/8 GPUs (ranks own contiguous
+index ranges) and the lowest index wins ties, so the selected schedule is
+the same for every GPU count.
+
+The winner feeds the reference solver API unchanged: ``SearchResult.schedule``
+is a valid warm start for ``start_session(warm=...)`` (solver.py:543-565), and
+``incumbent_events`` lists every strict improvement with its timestamp
+(the IncumbentEvent stream of solver.py:81-87, 435-449).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .engine import device_instance
+from .packing import decode_mask, decode_orders, encode_candidate
+
+
+@dataclass(frozen=True)
+class SearchConfig:
+    seed: int = 0
+    neighbours: int = 65536          # per round, all ranks together
+    shift_permille: int = 700        # SHIFT moves; the rest toggle offload bits
+    max_shift: int = 4
+
+
+@dataclass
+class Improvement:
+    round: int
+    makespan: int
+    timestamp: float                 # seconds since the search started
+    index: int
+
+
+@dataclass
+class SearchResult:
+    schedule: object
+    makespan: int
+    initial_makespan: int
+    rounds: int
+    evaluated: int
+    elapsed: float
+    improvements: list = field(default_factory=list)
+
+    def incumbent_events(self):
+        return [(imp.timestamp, imp.makespan) for imp in self.improvements]
+
+
+def shard_range(total: int, rank: int, world: int):
+    lo = total * rank // world
+    hi = total * (rank + 1) // world
+    return lo, hi - lo
+
+
+class LocalSearch:
+    def __init__(self, inst, stage_orders, offloaded, config: SearchConfig = SearchConfig(),
+                 device=None, group=None):
+        import torch
+        import torch.distributed as dist
+        self.inst = inst
+        self.cfg = config
+        self.di = device_instance(inst, device)
+        self.lib = self.di.lib
+        pk = self.di.packed
+        o, mk, _ = encode_candidate(pk, stage_orders, offloaded)
+        dev = torch.device("cuda", self.di.device)
+        self.inc_orders = torch.from_numpy(o.view(np.int16).copy()).to(dev)
+        self.inc_mask = torch.from_numpy(mk.view(np.int32).copy()).to(dev)
+        self.best_key = torch.empty(1, dtype=torch.int64, device=dev)
+        self.group = group
+        self.distributed = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.distributed else 0
+        self.world = dist.get_world_size(group) if self.distributed else 1
+        self.first, self.count = shard_range(config.neighbours, self.rank, self.world)
+        self.moves = N.MoveParams(config.seed & (2**64 - 1), config.shift_permille, config.max_shift)
+        res = self.di.evaluate(self.inc_orders.view(1, *self.inc_orders.shape),
+                               self.inc_mask.view(1, -1), peak=False)
+        if not int(res.flags[0].item()) & N.FLAG_FEASIBLE:
+            raise ValueError("the incumbent structure is not feasible")
+        self.makespan = int(res.makespan[0].item())
+        self.initial_makespan = self.makespan
+        self.round = 0
+        self.evaluated = 0
+        self.improvements = []
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.di.device).cuda_stream)
+
+    def launch_round(self, makespan_out=None):
+        """Enqueue one round's generate + evaluate + argmin (no host sync)."""
+        self.best_key.fill_(N.BEST_NONE)
+        desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round,
+                            self.first, self.count, self.moves)
+        N.check(self.lib.ps_search_round(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
+                                         C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None,
+                                         self._stream()))
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.best_key, op=dist.ReduceOp.MIN, group=self.group)
+
+    def finish_round(self, t0=None) -> bool:
+        """Read the combined key (host sync) and adopt a strict improvement."""
+        key = int(self.best_key.item())
+        r = self.round
+        self.round += 1
+        self.evaluated += self.cfg.neighbours
+        if key == N.BEST_NONE:
+            return False
+        span, idx = key >> 32, key & 0xFFFFFFFF
+        if span >= self.makespan:
+            return False
+        N.check(self.lib.ps_apply_move(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
+                                       C.c_void_p(self.inc_mask.data_ptr()), C.byref(self.moves),
+                                       r, idx, self._stream()))
+        self.makespan = span
+        self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
+        return True
+
+    def step(self, t0=None) -> bool:
+        self.launch_round()
+        return self.finish_round(t0)
+
+    def incumbent_structure(self):
+        pk = self.di.packed
+        o = self.inc_orders.cpu().numpy().view(np.uint16)
+        mk = self.inc_mask.cpu().numpy().view(np.uint32)
+        return decode_orders(pk, o), decode_mask(pk, mk)
+
+    def run(self, rounds: int | None = None, time_budget: float | None = None,
+            patience: int | None = None) -> SearchResult:
+        """Rounds until `rounds`, `time_budget` seconds or `patience` rounds without improvement."""
+        from .listsched import run_order
+        if rounds is None and time_budget is None:
+            raise ValueError("need rounds or time_budget")
+        t0 = time.perf_counter()
+        stale = 0
+        while True:
+            if rounds is not None and self.round >= rounds:
+                break
+            if time_budget is not None and time.perf_counter() - t0 >= time_budget:
+                break
+            if self.step(t0):
+                stale = 0
+            else:
+                stale += 1
+                if patience is not None and stale >= patience:
+                    break
+        elapsed = time.perf_counter() - t0
+        orders, off = self.incumbent_structure()
+        sched = run_order(self.inst, orders, off, device=self.di.device)
+        return SearchResult(sched, self.makespan, self.initial_makespan, self.round, self.evaluated,
+                            elapsed, list(self.improvements))
+
+    def materialize(self, first: int, count: int, rnd: int | None = None):
+        """Neighbours [first, first+count) of round `rnd` as full candidate tensors (for parity)."""
+        import torch
+        pk = self.di.packed
+        dev = self.inc_orders.device
+        orders = torch.empty((count, pk.num_stages, pk.order_stride), dtype=torch.int16, device=dev)
+        masks = torch.empty((count, pk.mask_words), dtype=torch.int32, device=dev)
+        desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(),
+                            self.round if rnd is None else rnd, first, count, self.moves)
+        N.check(self.lib.ps_materialize_moves(self.di.handle, C.byref(desc), C.c_void_p(orders.data_ptr()),
+                                              C.c_void_p(masks.data_ptr()), self._stream()))
+        return orders, masks
+
+
+def warm_start_search(inst, config: SearchConfig = SearchConfig(), rounds=None, time_budget=None,
+                      patience=None, device=None, group=None):
+    """best_feasible warm start, then GPU local search; returns SearchResult."""
+    from .heuristics import best_feasible
+    from .listsched import stage_order_of
+    s, _ = best_feasible(inst, device=device)
+    orders = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}
+    ls = LocalSearch(inst, orders, s.offloaded, config, device=device, group=group)
+    return ls.run(rounds=rounds, time_budget=time_budget, patience=patience)

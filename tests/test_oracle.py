@@ -1,0 +1,62 @@
+"""Pin the C oracle (oracle/ps_oracle.c) against reference-generated golden vectors (CPU)."""
+
+import numpy as np
+import pytest
+
+from _golden import CORPORA, case_arrays, corpus, split_trace
+from oracle.oracle import Oracle, philox4x32_10
+
+
+@pytest.mark.parametrize("name", CORPORA)
+def test_oracle_matches_reference_fixtures(name):
+    n_feasible = n_infeasible = 0
+    for inst, pk, cases in corpus(name):
+        orc = Oracle(pk)
+        for case in cases:
+            orders, mask, chans = case_arrays(pk, case)
+            r = orc.run(orders, mask, chans)
+            if "infeasible" in case:
+                assert r["flags"] == 2, case
+                stages = [i + 1 for i in range(pk.num_stages) if (r["blocked"] >> i) & 1]
+                assert stages == case["infeasible"]
+                n_infeasible += 1
+                continue
+            assert r["flags"] == 1
+            assert r["makespan"] == case["makespan"]
+            assert repr(r["bubble"]) == case["bubble"]          # bit-exact fp64
+            assert list(r["peak"]) == case["peak"]
+            comp, tr = split_trace(r["trace_code"], r["trace_start"])
+            assert comp == case["compute"]                      # commit order included
+            assert tr == case["transfers"]
+            n_feasible += 1
+    assert n_feasible > 0
+
+
+def test_oracle_batch_matches_single():
+    inst, pk, cases = corpus("ref_tests")[4]
+    orc = Oracle(pk)
+    arrs = [case_arrays(pk, c) for c in cases if "channel_orders" not in c]
+    orders = np.stack([a[0] for a in arrs])
+    masks = np.stack([a[1] for a in arrs])
+    out = orc.eval_batch(orders, masks, threads=3)
+    for k, (o, mk, _) in enumerate(arrs):
+        r = orc.run(o, mk)
+        assert out["makespan"][k] == r["makespan"]
+        assert out["flags"][k] == r["flags"]
+
+
+def test_philox_known_answers():
+    # Random123 known-answer vectors for philox4x32-10
+    assert philox4x32_10([0, 0, 0, 0], [0, 0]) == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    assert philox4x32_10([0xffffffff] * 4, [0xffffffff] * 2) == [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]
+    assert philox4x32_10([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0]) == \
+        [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+
+
+def test_malformed_candidates_are_flagged():
+    inst, pk, cases = corpus("ref_tests")[0]
+    orc = Oracle(pk)
+    orders, mask, _ = case_arrays(pk, cases[0])
+    bad = orders.copy()
+    bad[0, 1] = bad[0, 0]          # duplicate op
+    assert orc.run(bad, mask)["flags"] == 4
