@@ -1,0 +1,376 @@
+"""Benchmark: candidate schedules evaluated per second (BASELINE.json metric) on config 3.
+
+Workload (BASELINE.json configs[2]): Llama-style 7B
+synthetic stage profile, 8 stages x 64 microbatches, PCIe-bandwidth-limited
+offload, 65,536 candidates per round per GPU.  A step is one local-search
+round: every neighbour of the incumbent is generated on the device, evaluated
+by the sm_100a evaluator kernel, reduced to the best (makespan, index) key,
+all-reduced (MIN) across ranks, and the winner applied on improvement.
+Scaling is weak: each rank owns 65,536 neighbours of every round.
+
+Keys beyond the driver contract:
+  roofline      INT32-issue roofline of the evaluator kernel: algorithmic
+                work 10 int ops per committed event over the kernel's CUDA-event time, against
+                the INT32 peak measured live by ps_int32_probe on the same GPU.
+  cpu_baseline  the C restatement of the reference algorithm (oracle/, "port"), all host
+                threads, on the first neighbours of the same round; parity of that sample
+                with the GPU is checked and reported.
+  e2e           the same metric through ps_eval_batch_host: materialised candidates in
+                pinned host memory, copied in, evaluated, results copied out, every step.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "candidate schedules evaluated/sec"
+UNIT = "candidates/s"
+CONFIG = 3
+PER_GPU = 65536
+SEED = 20251005
+MOVES = dict(shift_permille=700, max_shift=4)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def build_incumbent_oracle(inst, pk, orc):
+    """AdaOffload structure found with the CPU port (first feasible fill of the back-off sequence)."""
+    import numpy as np
+    from paper_2510_05186_b200.heuristics import ada_backoff_sequence, filled_order
+    from paper_2510_05186_b200.packing import encode_candidate
+    off = frozenset(inst.offloadable_ops())
+    for fills in ada_backoff_sequence(inst):
+        o, mk, _ = encode_candidate(pk, {i: filled_order(inst, i, fills[i]) for i in range(1, pk.num_stages + 1)}, off)
+        r = orc.run(o, mk)
+        if r["flags"] == 1:
+            return o, mk, r["makespan"]
+    raise RuntimeError("no feasible AdaOffload structure")
+
+
+def calibrate_sample(orc, inc_o, inc_m, rnd, threads, target_s, cap):
+    """Neighbour count whose CPU evaluation takes about target_s seconds on `threads` threads."""
+    t = time.perf_counter()
+    orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"], rnd, 0, threads, threads)
+    per = (time.perf_counter() - t) / max(1, threads)     # seconds per candidate-thread
+    n = int(target_s / max(per, 1e-6) * threads)
+    return max(threads, min(cap, n))
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU restatement (oracle port), all host threads."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.packing import pack_instance
+    inst = workloads.CONFIGS[CONFIG]()
+    pk = pack_instance(inst)
+    orc = Oracle(pk)
+    threads = cpu_threads()
+    inc_o, inc_m, _ = build_incumbent_oracle(inst, pk, orc)
+    n = calibrate_sample(orc, inc_o, inc_m, 0, threads, args.ref_step_seconds, PER_GPU * max(1, args.gpus))
+    for w in range(args.warmup):
+        orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"], w, 0, n, threads)
+    times = []
+    for k in range(args.steps):
+        t = time.perf_counter()
+        orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"],
+                         args.warmup + k, 0, n, threads)
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = n * args.steps / total
+    sample = f"first {n} neighbours of each round (of {PER_GPU * max(1, args.gpus)}), config 3 AdaOffload incumbent"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": workload_config(args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world):
+    return {"workload": "config3: Llama-7B synthetic 8 stages x 64 microbatches, PCIe-limited offload, "
+                        "AdaOffload incumbent, 65536 neighbours/round/GPU",
+            "stages": 8, "microbatches": 64, "candidates_per_round": PER_GPU * world,
+            "candidates_per_gpu": PER_GPU, "parallelism": f"candidates sharded over {world} GPU(s)",
+            "l2": "flushed (256 MiB write) between timed steps",
+            "moves": MOVES, "seed": SEED}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=3.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2510_05186_b200 import _native as N, workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+
+    inst = workloads.CONFIGS[CONFIG]()
+    s0, gen_name = best_feasible(inst, device=local)
+    orders0 = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
+    cfg = SearchConfig(seed=SEED, neighbours=PER_GPU * world, **MOVES)
+    ls = LocalSearch(inst, orders0, s0.offloaded, cfg, device=local)
+    lib, di = ls.lib, ls.di
+    events_total = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def round_timed(ev_k0, ev_k1):
+        ls.best_key.fill_(N.BEST_NONE)
+        desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), ls.round, ls.first,
+                            ls.count, ls.moves, events_total.data_ptr())
+        ev_k0.record(stream)
+        N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()), None,
+                                    C.c_void_p(stream.cuda_stream)))
+        ev_k1.record(stream)
+        if world > 1:
+            dist.all_reduce(ls.best_key, op=dist.ReduceOp.MIN)
+        return ls.finish_round()
+
+    # ---- warm-up -------------------------------------------------------------------------------
+    for _ in range(args.warmup):
+        round_timed(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed search rounds -----------------------------------------------------------------------
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    improved = 0
+    events_total.zero_()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.fill_(k & 0xFF)          # evict L2 between steps (outside the step events)
+            es0, ek0, ek1, es1 = evs[k]
+            es0.record(stream)
+            improved += bool(round_timed(ek0, ek1))
+            es1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [evs[k][0].elapsed_time(evs[k][3]) for k in range(K)]
+    kern_ms = [evs[k][1].elapsed_time(evs[k][2]) for k in range(K)]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_s = float(total_ms.item()) / 1e3
+    value = cfg.neighbours * K / total_s
+    launches = 2 * K + improved        # evaluator main + overflow pass per round, apply_move per improvement
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": 1000 * total_s / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": workload_config(world), "clocks": clk.summary(), "gpu_launches": launches}
+
+    # ---- roofline: INT32 issue ----------------------------------------------------
+    ev_total = int(events_total.item())
+    kern_s = sum(kern_ms) / 1e3 / K
+    ops_per_launch = 10 * ev_total / K
+    probe = torch.zeros(1, dtype=torch.int64, device=dev)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    N.check(lib.ps_int32_probe(200, C.c_void_p(probe.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    probe.zero_()
+    p0.record(stream)
+    N.check(lib.ps_int32_probe(4000, C.c_void_p(probe.data_ptr()), C.c_void_p(stream.cuda_stream)))
+    p1.record(stream)
+    torch.cuda.synchronize()
+    int32_peak = int(probe.item()) / (p0.elapsed_time(p1) / 1e3) / 1e12
+    achieved = ops_per_launch / kern_s / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_eval_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    n_cand = cfg.neighbours // world
+    line["roofline"] = {
+        "bound": "int32-issue", "achieved": achieved, "peak": int32_peak, "unit": "Tops/s",
+        "frac": achieved / int32_peak, "traffic": traffic,
+        "kernel": "ps::eval_kernel<8,int,true,false> (move-encoded search round)",
+        "kernel_ms_per_launch": 1000 * kern_s, "kernel_share_of_step": sum(kern_ms) / sum(step_ms),
+        "events_per_launch": ev_total / K, "int_ops_per_event": 10,
+        "peak_source": "ps_int32_probe measured live on this GPU (IADD3/LOP3/IMAD chains)",
+        "hbm": {"algorithmic_bytes_per_launch": n_cand * (16 + 20 + 8 * inst.num_stages),
+                "achieved_gbs": n_cand * (16 + 20 + 8 * inst.num_stages) / kern_s / 1e9,
+                "peak_gbs": 6536.0, "note": "not the binding roof: move-encoded candidates"},
+        "note": "latency-bound discrete-event simulation; frac is INT32 issue utilisation"}
+
+    # ---- e2e through the C ABI with host buffers --------------------------------------------------
+    if not args.no_e2e:
+        pk = di.packed
+        orders_d, masks_d = ls.materialize(ls.first, n_cand)
+        torch.cuda.synchronize()
+        h_orders = torch.empty(orders_d.shape, dtype=torch.int16, pin_memory=True)
+        h_masks = torch.empty(masks_d.shape, dtype=torch.int32, pin_memory=True)
+        h_orders.copy_(orders_d)
+        h_masks.copy_(masks_d)
+        outs = dict(makespan=torch.empty(n_cand, dtype=torch.int64, pin_memory=True),
+                    bubble=torch.empty(n_cand, dtype=torch.float64, pin_memory=True),
+                    flags=torch.empty(n_cand, dtype=torch.int32, pin_memory=True),
+                    peak=torch.empty((n_cand, pk.num_stages), dtype=torch.int64, pin_memory=True),
+                    blocked=torch.empty(n_cand, dtype=torch.int32, pin_memory=True))
+        cb = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0)
+        rb = N.ResultBatch(outs["makespan"].data_ptr(), outs["bubble"].data_ptr(), outs["peak"].data_ptr(),
+                           outs["flags"].data_ptr(), outs["blocked"].data_ptr(), None, None, 0, None)
+        h2d = h_orders.numel() * 2 + h_masks.numel() * 4
+        d2h = n_cand * (8 + 8 + 4 + 4 + 8 * pk.num_stages)
+        for _ in range(args.warmup):
+            N.check(lib.ps_eval_batch_host(di.handle, C.byref(cb), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+        if world > 1:
+            dist.barrier()
+        e_ms = []
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            N.check(lib.ps_eval_batch_host(di.handle, C.byref(cb), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+            e_ms.append(1000 * (time.perf_counter() - t0))
+        e_tot = torch.tensor([sum(e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
+        e_s = float(e_tot.item()) / 1e3
+        line["e2e"] = {"value": n_cand * world * K / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * e_s / K,
+                       "api": "ps_eval_batch_host (pinned host buffers, copies inside the call)"}
+        e2e_flags = outs["flags"].numpy().copy()
+        e2e_span = outs["makespan"].numpy().copy()
+    else:
+        line["e2e"] = None
+
+    # ---- CPU baseline (rank 0, N=1): the oracle port on the first neighbours of one round ---------------
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle.oracle import Oracle
+        pk = di.packed
+        orc = Oracle(pk)
+        threads = cpu_threads()
+        inc_o = ls.inc_orders.cpu().numpy().view(np.uint16)
+        inc_m = ls.inc_mask.cpu().numpy().view(np.uint32)
+        rnd = ls.round
+        n = calibrate_sample(orc, inc_o, inc_m, rnd, threads, args.cpu_seconds, n_cand)
+        t0 = time.perf_counter()
+        best_cpu, ms_cpu = orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"],
+                                            rnd, 0, n, threads, want_makespans=True)
+        cpu_s = time.perf_counter() - t0
+        # parity of the sample: the GPU's makespans for the same neighbours of the same round
+        ms_gpu = torch.empty(n_cand, dtype=torch.int64, device=dev)
+        ls.best_key.fill_(N.BEST_NONE)
+        desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, n_cand, ls.moves, None)
+        N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
+                                    C.c_void_p(ms_gpu.data_ptr()), C.c_void_p(stream.cuda_stream)))
+        torch.cuda.synchronize()
+        gpu_ms = ms_gpu.cpu().numpy()
+        mism = int((gpu_ms[:n] != ms_cpu).sum())
+        line["cpu_baseline"] = {"value": n / cpu_s, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"first {n} of {n_cand} neighbours of round {rnd} "
+                                          f"(C restatement of listsched.run_order, oracle/ps_oracle.c)",
+                                "parity": {"checked": n, "makespan_mismatches": mism,
+                                           "best_key_equal_on_sample": bool(
+                                               int(ms_cpu[ms_cpu >= 0].min() if (ms_cpu >= 0).any() else -1) ==
+                                               int(gpu_ms[:n][gpu_ms[:n] >= 0].min() if (gpu_ms[:n] >= 0).any() else -1))}}
+        if not args.no_e2e:
+            line["e2e"]["feasible_share"] = float((e2e_flags & 1).mean())
+    line["search"] = {"initial_makespan": ls.initial_makespan, "final_makespan": ls.makespan,
+                      "warm_start": gen_name, "rounds": ls.round,
+                      "improvements": [[imp.round, imp.makespan] for imp in ls.improvements]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

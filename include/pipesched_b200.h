@@ -105,6 +105,7 @@ typedef struct ps_result_batch {
     uint32_t *trace_code;           /* [N][trace_stride] commit-ordered events (optional)         */
     int32_t *trace_start;           /* [N][trace_stride] start times of those events (optional)   */
     int32_t trace_stride;           /* >= info.max_events when trace arrays are given             */
+    int64_t *events_total;          /* device int64[1] (optional): += events committed by the batch */
 } ps_result_batch;
 
 /* Local-search neighbourhood: how a candidate index becomes a move. */
@@ -121,6 +122,7 @@ typedef struct ps_search_desc {
     int64_t first_index;            /* global index of this shard's first neighbour               */
     int64_t count;                  /* neighbours in this shard                                    */
     ps_move_params moves;
+    int64_t *events_total;          /* device int64[1] (optional): += events committed this round  */
 } ps_search_desc;
 
 const char *ps_version(void);

@@ -86,6 +86,7 @@ class ResultBatch(C.Structure):
         ("trace_code", C.c_void_p),
         ("trace_start", C.c_void_p),
         ("trace_stride", C.c_int32),
+        ("events_total", C.c_void_p),
     ]
 
 
@@ -105,6 +106,7 @@ class SearchDesc(C.Structure):
         ("first_index", C.c_int64),
         ("count", C.c_int64),
         ("moves", MoveParams),
+        ("events_total", C.c_void_p),
     ]
 
 

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -85,7 +86,7 @@ int next_pow2(int x) {
 }
 
 struct Plan {
-    int seg, segs, K, warps;
+    int K, warps;
     bool gstate;
     int cand_words, inc_words;
     LaunchCfg cfg;
@@ -104,39 +105,32 @@ int incumbent_words(const ps_instance *I, bool moves) {
     return (w + 3) & ~3;
 }
 
-cudaError_t occupancy(int seg, bool v64, bool moves, bool gstate, int block, size_t smem, int *n) {
-    switch (seg) {
-        case 2: return eval_occupancy<2>(v64, moves, gstate, block, smem, n);
-        case 4: return eval_occupancy<4>(v64, moves, gstate, block, smem, n);
-        case 8: return eval_occupancy<8>(v64, moves, gstate, block, smem, n);
-        case 16: return eval_occupancy<16>(v64, moves, gstate, block, smem, n);
-        default: return eval_occupancy<32>(v64, moves, gstate, block, smem, n);
-    }
+cudaError_t occupancy(bool v64, bool moves, bool gstate, int block, size_t smem, int *n) {
+    return v64 ? eval_occupancy<long long>(moves, gstate, block, smem, n) : eval_occupancy<int>(moves, gstate, block, smem, n);
 }
 
-cudaError_t launch(int seg, bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c,
-                   cudaStream_t s) {
-    switch (seg) {
-        case 2: return eval_launch<2>(v64, moves, gstate, p, c, s);
-        case 4: return eval_launch<4>(v64, moves, gstate, p, c, s);
-        case 8: return eval_launch<8>(v64, moves, gstate, p, c, s);
-        case 16: return eval_launch<16>(v64, moves, gstate, p, c, s);
-        default: return eval_launch<32>(v64, moves, gstate, p, c, s);
-    }
+cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s) {
+    return v64 ? eval_launch<long long>(moves, gstate, p, c, s) : eval_launch<int>(moves, gstate, p, c, s);
 }
 
-// Shared-memory plan for the main pass: window K=32 (or 5m when smaller: cannot overflow),
-// as many warps per block as fit; state moves to global memory only when one warp cannot fit.
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// Shared-memory plan for the main pass: one candidate per warp, ledger window K (16 by default, or
+// the whole 5m ledger when that is smaller and cannot overflow), as many warps per block as fit;
+// state moves to global memory only when a single warp's state does not fit.
 int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
-    pl->seg = std::max(2, next_pow2(I->P));
-    pl->segs = 32 / pl->seg;
-    pl->K = std::min(32, next_pow2(5 * I->m));
+    pl->K = std::min(next_pow2(std::max(4, env_int("PS_WINDOW", 16))), next_pow2(5 * I->m));
     pl->cand_words = words_per_candidate(I, pl->K);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
     pl->warps = 4;
+    const int max_warps = std::max(1, std::min(4, env_int("PS_WARPS_PER_BLOCK", 4)));
     for (int w : {4, 2, 1}) {
-        size_t smem = (size_t)(pl->inc_words + w * pl->segs * pl->cand_words) * 4;
+        if (w > max_warps) continue;
+        size_t smem = (size_t)(pl->inc_words + w * pl->cand_words) * 4;
         if (smem <= (size_t)I->max_smem_optin) {
             pl->warps = w;
             pl->gstate = false;
@@ -149,20 +143,17 @@ int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
         return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
     pl->cfg.block = 32 * pl->warps;
     int per_sm = 0;
-    cudaError_t e = occupancy(pl->seg, I->v64, moves, pl->gstate, pl->cfg.block, pl->cfg.smem, &per_sm);
+    cudaError_t e = occupancy(I->v64, moves, pl->gstate, pl->cfg.block, pl->cfg.smem, &per_sm);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     if (per_sm < 1) per_sm = 1;
-    int64_t per_block = (int64_t)pl->warps * pl->segs;
-    int64_t want = (N + per_block - 1) / per_block;
+    int64_t want = (N + pl->warps - 1) / pl->warps;
     pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * I->num_sms));
-    pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * per_block * pl->cand_words * 4 : 0;
+    pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * pl->warps * pl->cand_words * 4 : 0;
     return PS_OK;
 }
 
 // Overflow pass: window of 5m points per stage (the whole ledger), state in global memory.
 int plan_retry(const ps_instance *I, bool moves, Plan *pl) {
-    pl->seg = std::max(2, next_pow2(I->P));
-    pl->segs = 32 / pl->seg;
     pl->K = next_pow2(5 * I->m);
     pl->cand_words = words_per_candidate(I, pl->K);
     pl->inc_words = incumbent_words(I, moves);
@@ -171,7 +162,7 @@ int plan_retry(const ps_instance *I, bool moves, Plan *pl) {
     pl->cfg.block = 32;
     pl->cfg.smem = (size_t)pl->inc_words * 4;
     pl->cfg.grid = I->num_sms;
-    pl->scratch_bytes = (size_t)pl->cfg.grid * pl->segs * pl->cand_words * 4;
+    pl->scratch_bytes = (size_t)pl->cfg.grid * pl->cand_words * 4;
     return PS_OK;
 }
 
@@ -205,7 +196,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s) {
     p.cand_words = main_pl.cand_words;
     p.inc_words = main_pl.inc_words;
     p.gstate = scratch;
-    cudaError_t e = launch(main_pl.seg, I->v64, moves, main_pl.gstate, p, main_pl.cfg, s);
+    cudaError_t e = launch(I->v64, moves, main_pl.gstate, p, main_pl.cfg, s);
     if (e != cudaSuccess) return cuda_fail(e, "evaluator launch");
 
     EvalParams q = p;
@@ -217,7 +208,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s) {
     q.cand_words = retry_pl.cand_words;
     q.inc_words = retry_pl.inc_words;
     q.gstate = scratch2;
-    e = launch(retry_pl.seg, I->v64, moves, true, q, retry_pl.cfg, s);
+    e = launch(I->v64, moves, true, q, retry_pl.cfg, s);
     if (e != cudaSuccess) return cuda_fail(e, "evaluator overflow launch");
     if (scratch) PS_CUDA(cudaFreeAsync(scratch, s));
     PS_CUDA(cudaFreeAsync(scratch2, s));
@@ -460,7 +451,7 @@ int ps_instance_get_info(const ps_instance *I, ps_instance_info *o) {
     o->value_bits = I->v64 ? 64 : 32;
     o->memory_unit = I->unit;
     o->busy_time = I->busy;
-    o->lanes_per_candidate = std::max(2, next_pow2(I->P));
+    o->lanes_per_candidate = 32;
     o->device = I->device;
     return PS_OK;
 }
@@ -494,6 +485,7 @@ int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_
     p.tcode = r->trace_code;
     p.tstart = r->trace_start;
     p.tstride = r->trace_stride;
+    p.events_total = (unsigned long long *)r->events_total;
     return run_eval(I, p, false, (cudaStream_t)stream);
 }
 
@@ -509,6 +501,7 @@ int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_re
     const size_t n_peak = r->peak ? (size_t)N * I->P * 8 : 0;
     const size_t n_tr = r->trace_code ? (size_t)N * r->trace_stride * 4 : 0;
     const size_t n_blk = r->blocked ? (size_t)N * 4 : 0;
+    if (r->events_total) return fail(PS_ERR_INVALID, "events_total is a device counter: use ps_eval_batch");
     // one device arena: inputs, then outputs
     size_t off[10], total = 0;
     size_t sizes[10] = {n_ord, n_mask, n_chan, (size_t)N * 8, (size_t)N * 8, n_peak, (size_t)N * 4, n_blk, n_tr, n_tr};
@@ -570,6 +563,7 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.max_shift = d->moves.max_shift;
     p.makespan = makespan_out;
     p.best_key = (long long *)best_key;
+    p.events_total = (unsigned long long *)d->events_total;
     return run_eval(I, p, true, (cudaStream_t)stream);
 }
 

@@ -1,4 +1,4 @@
-// ps_launch.h — host-side launch interface of the evaluator variants (one TU per SEG).
+// ps_launch.h — host-side launch interface of the evaluator variants (one TU per ledger width).
 #pragma once
 #include <cuda_runtime.h>
 #include "ps_eval.cuh"
@@ -10,11 +10,10 @@ struct LaunchCfg {
     size_t smem;
 };
 
-// Variant = (SEG, 64-bit ledger values, move-encoded candidates, state in global memory).
-template <int SEG>
-cudaError_t eval_launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg cfg,
-                        cudaStream_t stream);
-template <int SEG>
-cudaError_t eval_occupancy(bool v64, bool moves, bool gstate, int block, size_t smem, int *blocks_per_sm);
+// Variant = (ledger value type V, move-encoded candidates, state in global memory).
+template <typename V>
+cudaError_t eval_launch(bool moves, bool gstate, const EvalParams &p, LaunchCfg cfg, cudaStream_t stream);
+template <typename V>
+cudaError_t eval_occupancy(bool moves, bool gstate, int block, size_t smem, int *blocks_per_sm);
 
 }  // namespace ps
