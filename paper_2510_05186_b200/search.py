@@ -60,9 +60,32 @@ class SearchResult:
 
 
 def shard_range(total: int, rank: int, world: int):
+    """Contiguous global-index range [first, first + count) owned by `rank`."""
     lo = total * rank // world
     hi = total * (rank + 1) // world
     return lo, hi - lo
+
+
+def pack_key(makespan: int, index: int) -> int:
+    """(makespan << 32 | index): the minimum is the best makespan, lowest index on ties."""
+    return (int(makespan) << 32) | (int(index) & 0xFFFFFFFF)
+
+
+def unpack_key(key: int):
+    return key >> 32, key & 0xFFFFFFFF
+
+
+def combine_keys(key_tensor, group=None):
+    """All-reduce(MIN) of each rank's best key: one 8-byte collective per round (NCCL on GPUs)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(key_tensor, op=dist.ReduceOp.MIN, group=group)
+    return key_tensor
+
+
+def improves(key: int, incumbent_makespan: int) -> bool:
+    """Only strict improvements replace the incumbent (solver.py:437 convention)."""
+    return key != N.BEST_NONE and unpack_key(key)[0] < incumbent_makespan
 
 
 class LocalSearch:
@@ -109,8 +132,7 @@ class LocalSearch:
                                          C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None,
                                          self._stream()))
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.best_key, op=dist.ReduceOp.MIN, group=self.group)
+            combine_keys(self.best_key, self.group)
 
     def finish_round(self, t0=None) -> bool:
         """Read the combined key (host sync) and adopt a strict improvement."""
@@ -118,11 +140,9 @@ class LocalSearch:
         r = self.round
         self.round += 1
         self.evaluated += self.cfg.neighbours
-        if key == N.BEST_NONE:
+        if not improves(key, self.makespan):
             return False
-        span, idx = key >> 32, key & 0xFFFFFFFF
-        if span >= self.makespan:
-            return False
+        span, idx = unpack_key(key)
         N.check(self.lib.ps_apply_move(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
                                        C.c_void_p(self.inc_mask.data_ptr()), C.byref(self.moves),
                                        r, idx, self._stream()))

@@ -1,0 +1,118 @@
+"""GPU local search vs its CPU restatement (oracle/ps_oracle.c): moves, rounds, whole searches."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SEED, PERMILLE, MAXSHIFT = 11, 700, 4
+
+
+def _setup(cfg=2):
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+    inst = workloads.CONFIGS[cfg]()
+    s, _ = best_feasible(inst)
+    orders = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}
+    return inst, orders, s.offloaded, LocalSearch, SearchConfig
+
+
+def test_move_decoding_matches_the_cpu_restatement(cuda_ok):
+    from oracle.oracle import Oracle
+    inst, orders, off, LocalSearch, SearchConfig = _setup()
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=512, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    orc = Oracle(ls.di.packed)
+    inc_o = ls.inc_orders.cpu().numpy().view(np.uint16)
+    inc_m = ls.inc_mask.cpu().numpy().view(np.uint32)
+    for rnd in (0, 3):
+        o, mk = ls.materialize(0, 512, rnd)
+        o = o.cpu().numpy().view(np.uint16)
+        mk = mk.cpu().numpy().view(np.uint32)
+        kinds = set()
+        for idx in range(512):
+            t, oo, mm = orc.neighbour(inc_o, inc_m, SEED, PERMILLE, MAXSHIFT, rnd, idx)
+            kinds.add(t)
+            assert (oo == o[idx]).all(), idx
+            assert (mm == mk[idx]).all(), idx
+        assert kinds == {0, 1, 2}
+
+
+def test_search_round_matches_cpu_round(cuda_ok):
+    import torch
+    import ctypes as C
+    from oracle.oracle import Oracle
+    from paper_2510_05186_b200 import _native as N
+    inst, orders, off, LocalSearch, SearchConfig = _setup(3)
+    n = 2048
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    ms = torch.empty(n, dtype=torch.int64, device="cuda")
+    ls.launch_round(ms)
+    torch.cuda.synchronize()
+    orc = Oracle(ls.di.packed)
+    best, want = orc.search_round(ls.inc_orders.cpu().numpy().view(np.uint16),
+                                  ls.inc_mask.cpu().numpy().view(np.uint32), SEED, PERMILLE, MAXSHIFT,
+                                  0, 0, n, want_makespans=True)
+    assert (ms.cpu().numpy() == want).all()
+    assert int(ls.best_key.item()) == best
+
+
+def test_identical_best_schedule_for_equal_budgets(cuda_ok):
+    """A whole search: the GPU and the CPU restatement adopt the same moves and end identical."""
+    from oracle.oracle import Oracle
+    inst, orders, off, LocalSearch, SearchConfig = _setup(2)
+    n, rounds = 1024, 6
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    orc = Oracle(ls.di.packed)
+    inc_o = ls.inc_orders.cpu().numpy().view(np.uint16)
+    inc_m = ls.inc_mask.cpu().numpy().view(np.uint32)
+    span = ls.makespan
+    cpu_trail = []
+    for rnd in range(rounds):
+        best, _ = orc.search_round(inc_o, inc_m, SEED, PERMILLE, MAXSHIFT, rnd, 0, n)
+        if best != (1 << 63) - 1 and (best >> 32) < span:
+            span = best >> 32
+            _, inc_o, inc_m = orc.neighbour(inc_o, inc_m, SEED, PERMILLE, MAXSHIFT, rnd, best & 0xFFFFFFFF)
+            cpu_trail.append((rnd, span))
+    res = ls.run(rounds=rounds)
+    assert [(imp.round, imp.makespan) for imp in res.improvements] == cpu_trail
+    assert res.makespan == span
+    assert (ls.inc_orders.cpu().numpy().view(np.uint16) == inc_o).all()
+    assert (ls.inc_mask.cpu().numpy().view(np.uint32) == inc_m).all()
+    from paper_2510_05186_b200 import makespan, validate
+    assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == span
+
+
+def test_generators_match_reference_outputs(cuda_ok):
+    """Batched warm-start generation vs the reference generators (tests/golden/generators.json.gz)."""
+    import gzip
+    import json
+    from pathlib import Path
+    from paper_2510_05186_b200 import instance_from_dict, makespan, memory_trace
+    from paper_2510_05186_b200.heuristics import best_feasible, generate_all, ada_fill_counts
+    from paper_2510_05186_b200.listsched import stage_order_of
+    g = json.load(gzip.open(Path(__file__).parent / "golden" / "generators.json.gz", "rt"))
+    for row in g["generators"]:
+        inst = instance_from_dict(row["instance"])
+        assert [ada_fill_counts(inst)[i] for i in range(1, inst.num_stages + 1)] == row["ada_fills"]
+        out = generate_all(inst)
+        for name, want in row["generators"].items():
+            got = out[name]
+            if "infeasible" in want:
+                assert isinstance(got, Exception), name
+                continue
+            assert makespan(got, inst) == want["makespan"], name
+            enc = [[((op.microbatch - 1) << 2) | int(op.kind) for op in stage_order_of(got, i)]
+                   for i in range(1, inst.num_stages + 1)]
+            assert enc == want["orders"], name
+            assert sorted([op.stage, op.microbatch] for op in got.offloaded) == want["offloaded"]
+            assert [memory_trace(got, inst).peak[i] for i in range(1, inst.num_stages + 1)] == want["peak"]
+        if row["best_feasible"] is None:
+            continue
+        s, name = best_feasible(inst)
+        assert name == row["best_feasible"]["name"]
+        assert makespan(s, inst) == row["best_feasible"]["makespan"]
