@@ -210,7 +210,8 @@ def main():
     def round_timed(ev_k0, ev_k1):
         ls.best_key.fill_(N.BEST_NONE)
         desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), ls.round, ls.first,
-                            ls.count, ls.moves, events_total.data_ptr())
+                            ls.count, ls.moves, events_total.data_ptr(),
+                            ls.base.handle if ls.base is not None else None)
         ev_k0.record(stream)
         N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()), None,
                                     C.c_void_p(stream.cuda_stream)))
@@ -303,7 +304,8 @@ def main():
                     flags=torch.empty(n_cand, dtype=torch.int32, pin_memory=True),
                     peak=torch.empty((n_cand, pk.num_stages), dtype=torch.int64, pin_memory=True),
                     blocked=torch.empty(n_cand, dtype=torch.int32, pin_memory=True))
-        cb = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0)
+        cb = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0,
+                         ls.base.handle if ls.base is not None else None)
         rb = N.ResultBatch(outs["makespan"].data_ptr(), outs["bubble"].data_ptr(), outs["peak"].data_ptr(),
                            outs["flags"].data_ptr(), outs["blocked"].data_ptr(), None, None, 0, None)
         h2d = h_orders.numel() * 2 + h_masks.numel() * 4
@@ -348,7 +350,8 @@ def main():
         # parity of the sample: the GPU's makespans for the same neighbours of the same round
         ms_gpu = torch.empty(n_cand, dtype=torch.int64, device=dev)
         ls.best_key.fill_(N.BEST_NONE)
-        desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, n_cand, ls.moves, None)
+        desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, n_cand, ls.moves, None,
+                            ls.base.handle if ls.base is not None else None)
         N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
                                     C.c_void_p(ms_gpu.data_ptr()), C.c_void_p(stream.cuda_stream)))
         torch.cuda.synchronize()

@@ -55,6 +55,10 @@ extern "C" {
 #define PS_MAX_MICROBATCHES 4096
 
 typedef struct ps_instance ps_instance;
+/* A recorded base candidate: its simulation checkpointed every few steps, so candidates that share
+   a prefix of decisions with it resume from the last checkpoint before they diverge (exact; see
+   DESIGN.md §3.5).  Created per instance, re-recorded whenever the base changes. */
+typedef struct ps_base ps_base;
 
 /* Dense instance tables, host memory, copied by ps_instance_create. */
 typedef struct ps_instance_desc {
@@ -93,6 +97,8 @@ typedef struct ps_cand_batch {
     const uint32_t *offload_mask;   /* [N][mask_words]                                               */
     const uint32_t *channel_orders; /* [N][G][chan_stride] or NULL = derived (greedy) channel mode   */
     int32_t chan_stride;
+    const ps_base *base;            /* optional recorded base (derived mode, no trace): shared
+                                       prefixes are restored instead of re-simulated            */
 } ps_cand_batch;
 
 /* Per-candidate outputs, device memory.  Optional arrays may be NULL. */
@@ -123,6 +129,7 @@ typedef struct ps_search_desc {
     int64_t count;                  /* neighbours in this shard                                    */
     ps_move_params moves;
     int64_t *events_total;          /* device int64[1] (optional): += events committed this round  */
+    const ps_base *base;            /* optional: the incumbent recorded with ps_base_record        */
 } ps_search_desc;
 
 const char *ps_version(void);
@@ -131,6 +138,12 @@ const char *ps_last_error(void);
 int ps_instance_create(const ps_instance_desc *desc, int device, ps_instance **out);
 int ps_instance_destroy(ps_instance *inst);
 int ps_instance_get_info(const ps_instance *inst, ps_instance_info *out);
+
+/* Base recording for prefix sharing.  ps_base_record copies the candidate (device buffers
+   [P][order_stride] and [mask_words]) and simulates it once, checkpointing as it goes. */
+int ps_base_create(const ps_instance *inst, ps_base **out);
+int ps_base_destroy(ps_base *base);
+int ps_base_record(ps_base *base, const uint16_t *orders, const uint32_t *mask, void *stream);
 
 /* Evaluate N candidates (device buffers) on `stream` (a cudaStream_t, NULL = legacy default). */
 int ps_eval_batch(const ps_instance *inst, const ps_cand_batch *batch,

@@ -12,7 +12,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpipesched_b200.so"
+LIB_PATH = Path(os.environ.get("PS_LIBRARY") or Path(__file__).resolve().parent / "_lib" / "libpipesched_b200.so")
 
 PS_OK = 0
 FLAG_FEASIBLE = 1
@@ -73,6 +73,7 @@ class CandBatch(C.Structure):
         ("offload_mask", C.c_void_p),
         ("channel_orders", C.c_void_p),
         ("chan_stride", C.c_int32),
+        ("base", C.c_void_p),
     ]
 
 
@@ -107,6 +108,7 @@ class SearchDesc(C.Structure):
         ("count", C.c_int64),
         ("moves", MoveParams),
         ("events_total", C.c_void_p),
+        ("base", C.c_void_p),
     ]
 
 
@@ -123,6 +125,9 @@ EXPORTS = {
     "ps_apply_move": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(MoveParams),
                                 C.c_uint64, C.c_uint64, C.c_void_p]),
     "ps_int32_probe": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p]),
+    "ps_base_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "ps_base_destroy": (C.c_int, [C.c_void_p]),
+    "ps_base_record": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

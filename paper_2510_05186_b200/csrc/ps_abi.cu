@@ -30,6 +30,18 @@ struct ps_instance {
     std::vector<uint8_t> h_offloadable;   // [P][m]
 };
 
+struct ps_base {
+    const ps_instance *inst;
+    int K, cand_words, ck_words, ck_interval, ck_max;
+    uint32_t *ck;       // [ck_max][ck_words]
+    uint32_t *cstep;    // [P][L]
+    uint32_t *fstep;    // [P][m]
+    int32_t *info;      // [4]
+    int64_t *res;       // [2 + P]
+    uint16_t *orders;   // [P][stride]
+    uint32_t *mask;     // [mask_words]
+};
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -95,7 +107,7 @@ struct Plan {
 
 int words_per_candidate(const ps_instance *I, int K) {
     int vw = I->v64 ? 2 : 1;
-    int w = I->P * K * (vw + 1) + 2 * I->P * I->m + 3 * I->P * I->MW;
+    int w = I->P * 2 * K * (vw + 1) + 2 * I->P * I->m + 3 * I->P * I->MW;
     return (w + 3) & ~3;
 }
 
@@ -109,8 +121,9 @@ cudaError_t occupancy(bool v64, bool moves, bool gstate, int block, size_t smem,
     return v64 ? eval_occupancy<long long>(moves, gstate, block, smem, n) : eval_occupancy<int>(moves, gstate, block, smem, n);
 }
 
-cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s) {
-    return v64 ? eval_launch<long long>(moves, gstate, p, c, s) : eval_launch<int>(moves, gstate, p, c, s);
+cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s,
+                   bool record = false) {
+    return v64 ? eval_launch<long long>(moves, gstate, record, p, c, s) : eval_launch<int>(moves, gstate, record, p, c, s);
 }
 
 int env_int(const char *name, int dflt) {
@@ -118,11 +131,13 @@ int env_int(const char *name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-// Shared-memory plan for the main pass: one candidate per warp, ledger window K (16 by default, or
+// Shared-memory plan for the main pass: one candidate per warp, ledger window K (12 by default, or
 // the whole 5m ledger when that is smaller and cannot overflow), as many warps per block as fit;
 // state moves to global memory only when a single warp's state does not fit.
+int window_size(const ps_instance *I) { return std::min(std::max(4, env_int("PS_WINDOW", 12)), 5 * I->m); }
+
 int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
-    pl->K = std::min(next_pow2(std::max(4, env_int("PS_WINDOW", 16))), next_pow2(5 * I->m));
+    pl->K = window_size(I);
     pl->cand_words = words_per_candidate(I, pl->K);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
@@ -154,7 +169,7 @@ int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
 
 // Overflow pass: window of 5m points per stage (the whole ledger), state in global memory.
 int plan_retry(const ps_instance *I, bool moves, Plan *pl) {
-    pl->K = next_pow2(5 * I->m);
+    pl->K = 5 * I->m;
     pl->cand_words = words_per_candidate(I, pl->K);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
@@ -173,13 +188,29 @@ void fill_instance(const ps_instance *I, EvalParams *p) {
     p->proc = I->d_proc; p->vals = I->d_vals; p->limit = I->d_limit; p->chan = I->d_chan;
 }
 
+void attach_base(const ps_base *B, EvalParams *p) {
+    p->ck = B->ck;
+    p->cstep = B->cstep;
+    p->fstep = B->fstep;
+    p->base_info = B->info;
+    p->base_res = B->res;
+    p->base_orders = B->orders;
+    p->base_mask = B->mask;
+    p->ck_interval = B->ck_interval;
+    p->ck_words = B->ck_words;
+    p->ck_max = B->ck_max;
+}
+
 // Main pass + overflow pass on one stream; all scratch is stream-ordered.
-int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s) {
+int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr) {
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
     Plan main_pl, retry_pl;
     int rc = plan_main(I, moves, p.N, &main_pl);
     if (rc) return rc;
+    // a base is usable when the main pass runs in shared memory with the window it was recorded with
+    if (B && B->inst == I && !main_pl.gstate && B->K == main_pl.K && p.chorders == nullptr && p.tcode == nullptr)
+        attach_base(B, &p);
     plan_retry(I, moves, &retry_pl);
     int32_t *ovf = nullptr;
     uint32_t *scratch = nullptr, *scratch2 = nullptr;
@@ -200,6 +231,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "evaluator launch");
 
     EvalParams q = p;
+    q.ck = nullptr;           // the overflow pass re-simulates from scratch with the full ledger
     q.work_list = ovf + 1;
     q.work_count = ovf;
     q.ovf_list = nullptr;     // the full-ledger window cannot overflow
@@ -456,6 +488,83 @@ int ps_instance_get_info(const ps_instance *I, ps_instance_info *o) {
     return PS_OK;
 }
 
+int ps_base_create(const ps_instance *I, ps_base **out) {
+    if (!I || !out) return fail(PS_ERR_INVALID, "null argument");
+    *out = nullptr;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    ps_base *B = new (std::nothrow) ps_base();
+    if (!B) return fail(PS_ERR_NOMEM, "host allocation");
+    B->inst = I;
+    B->K = window_size(I);
+    B->cand_words = words_per_candidate(I, B->K);
+    B->ck_words = B->cand_words + 32 * CK_REGW;
+    B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 32))));
+    B->ck_max = 5 * I->P * I->m / B->ck_interval + 2;
+    cudaError_t e = cudaMalloc((void **)&B->ck, (size_t)B->ck_max * B->ck_words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->cstep, (size_t)I->P * I->L * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->fstep, (size_t)I->P * I->m * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->info, 4 * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->res, (size_t)(2 + I->P) * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->orders, (size_t)I->P * I->stride * 2);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->mask, (size_t)I->mask_words * 4);
+    if (e == cudaSuccess) e = cudaMemset(B->info, 0xFF, 4 * sizeof(int32_t));   // -1: nothing recorded
+    if (e != cudaSuccess) {
+        ps_base_destroy(B);
+        return fail(PS_ERR_NOMEM, "base workspace: %s", cudaGetErrorString(e));
+    }
+    *out = B;
+    return PS_OK;
+}
+
+int ps_base_destroy(ps_base *B) {
+    if (!B) return PS_OK;
+    DeviceGuard guard(B->inst->device);
+    cudaFree(B->ck);
+    cudaFree(B->cstep);
+    cudaFree(B->fstep);
+    cudaFree(B->info);
+    cudaFree(B->res);
+    cudaFree(B->orders);
+    cudaFree(B->mask);
+    delete B;
+    return PS_OK;
+}
+
+int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, void *stream) {
+    if (!B || !orders || !mask) return fail(PS_ERR_INVALID, "null argument");
+    const ps_instance *I = B->inst;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    PS_CUDA(cudaMemcpyAsync(B->orders, orders, (size_t)I->P * I->stride * 2, cudaMemcpyDeviceToDevice, s));
+    PS_CUDA(cudaMemcpyAsync(B->mask, mask, (size_t)I->mask_words * 4, cudaMemcpyDeviceToDevice, s));
+    PS_CUDA(cudaMemsetAsync(B->cstep, 0xFF, (size_t)I->P * I->L * 4, s));
+    PS_CUDA(cudaMemsetAsync(B->fstep, 0xFF, (size_t)I->P * I->m * 4, s));
+    EvalParams p;
+    memset(&p, 0, sizeof p);
+    fill_instance(I, &p);
+    p.N = 1;
+    p.orders = B->orders;
+    p.masks = B->mask;
+    p.K = B->K;
+    p.cand_words = B->cand_words;
+    p.inc_words = 0;
+    attach_base(B, &p);
+    LaunchCfg cfg;
+    cfg.grid = 1;
+    cfg.block = 32;
+    cfg.smem = (size_t)B->cand_words * 4;
+    if (cfg.smem > (size_t)I->max_smem_optin) {
+        // too large to record in shared memory: leave the base unusable (evaluations run in full)
+        PS_CUDA(cudaMemsetAsync(B->info, 0xFF, 4 * sizeof(int32_t), s));
+        return PS_OK;
+    }
+    cudaError_t e = launch(I->v64, false, false, p, cfg, s, true);
+    if (e != cudaSuccess) return cuda_fail(e, "base recording launch");
+    return PS_OK;
+}
+
 int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
     if (b->num_candidates < 0) return fail(PS_ERR_INVALID, "negative candidate count");
@@ -486,7 +595,7 @@ int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_
     p.tstart = r->trace_start;
     p.tstride = r->trace_stride;
     p.events_total = (unsigned long long *)r->events_total;
-    return run_eval(I, p, false, (cudaStream_t)stream);
+    return run_eval(I, p, false, (cudaStream_t)stream, b->base);
 }
 
 int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
@@ -564,7 +673,7 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.makespan = makespan_out;
     p.best_key = (long long *)best_key;
     p.events_total = (unsigned long long *)d->events_total;
-    return run_eval(I, p, true, (cudaStream_t)stream);
+    return run_eval(I, p, true, (cudaStream_t)stream, d->base);
 }
 
 int ps_materialize_moves(const ps_instance *I, const ps_search_desc *d, uint16_t *orders_out, uint32_t *mask_out,

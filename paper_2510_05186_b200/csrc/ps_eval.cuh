@@ -73,11 +73,25 @@ struct EvalParams {
     const int32_t *work_list;
     const int32_t *work_count;
     // per-candidate state
-    int K;                   // ledger window capacity (power of two)
+    int K;                   // ledger window capacity in merged breakpoints (2K slots per stage)
     int cand_words;          // 32-bit words of one candidate's state
     int inc_words;           // 32-bit words of the block-shared incumbent (move mode)
     uint32_t *gstate;        // GSTATE scratch
+    // prefix sharing against a recorded base candidate
+    int ck_interval;         // steps between checkpoints (power of two)
+    int ck_words;            // words per checkpoint: cand_words + 32 * CK_REGW
+    int ck_max;              // checkpoint capacity
+    uint32_t *ck;            // [ck_max][ck_words]; NULL = no base
+    uint32_t *cstep;         // [P][L] step at which the base commits stage i's q-th op (~0 = never)
+    uint32_t *fstep;         // [P][m] step at which the base commits F(i, j)
+    int32_t *base_info;      // [0] checkpoints (-1 unusable) [1] flags [2] events [3] blocked
+    int64_t *base_res;       // [0] makespan [1] bubble bits [2 .. 2+P) peaks
+    const uint16_t *base_orders;   // [P][stride] (materialised candidates)
+    const uint32_t *base_mask;     // [mask_words]
 };
+
+constexpr int CK_REGW = 20;          // per-lane register words saved in a checkpoint
+constexpr uint32_t NEVER = 0xFFFFFFFFu;
 
 template <typename V>
 __device__ __forceinline__ V ldv(const void *base, int idx) {
@@ -88,14 +102,20 @@ __device__ __forceinline__ bool key_less(uint32_t ah, uint32_t al, uint32_t bh, 
     return ah < bh || (ah == bh && al < bl);
 }
 
-template <typename V, bool MOVES, bool GSTATE>
-__global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
+// 64 registers per thread (8 blocks of 4 warps per SM) measured best on B200 for the
+// shared-memory variants (tools/kexp.py); the global-state variant keeps its registers.
+#ifndef PS_MIN_BLOCKS
+#define PS_MIN_BLOCKS 8
+#endif
+
+template <typename V, bool MOVES, bool GSTATE, bool REC>
+__global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval_kernel(const EvalParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
-    const int P = p.P, m = p.m, L = p.L, MW = p.MW, K = p.K, KM = p.K - 1;
+    const int P = p.P, m = p.m, L = p.L, MW = p.MW, K = p.K;
     const int i = lane;                               // the stage this lane owns
     const bool has_stage = i < P;
     const int is = has_stage ? i : 0;
@@ -116,9 +136,9 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
     const long long slot = (long long)blockIdx.x * nwarps + warp;
     const long long nslots = (long long)gridDim.x * nwarps;
     uint32_t *cb = GSTATE ? p.gstate + (size_t)slot * p.cand_words : smem + p.inc_words + (size_t)warp * p.cand_words;
-    V *wd = reinterpret_cast<V *>(cb) + (size_t)is * K;                 // own ledger window: deltas
-    uint32_t *wt = cb + (size_t)P * K * VW + (size_t)is * K;              // own ledger window: times
-    uint32_t *A = cb + (size_t)P * K * (VW + 1);         // [P][m] F end, then B end   (time<<2 | state)
+    V *wu = reinterpret_cast<V *>(cb) + (size_t)is * 2 * K;             // own ledger window: usage after
+    uint32_t *wt = cb + (size_t)P * 2 * K * VW + (size_t)is * 2 * K;      // own ledger window: times
+    uint32_t *A = cb + (size_t)P * 2 * K * (VW + 1);     // [P][m] F end, then B end   (time<<2 | state)
     uint32_t *X = A + (size_t)P * m;                      // [P][m] offload end, then reload end
     uint32_t *offm = X + (size_t)P * m;                   // [P][MW] offloaded bits
     uint32_t *poff = offm + (size_t)P * MW;               // [P][MW] pending offload requests
@@ -163,12 +183,12 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
     uint32_t tkh = KEY_NONE, tkl = KEY_NONE;   // cached best transfer key of this stage
     bool cdirty = false, tdirty = false, ovf = false;
     V base = 0, top = 0, peak = 0;
-    int wh = 0, wn = 0;
+    int ws = 0, we = 0;
     int n_poff = 0, n_prel = 0, n_unrel = 0;   // pending offloads / reloads / offloaded not yet reloaded
     V rF = V(-1), rG = V(-1);                  // earliest_fit cache, valid until the ledger changes
     int tauF = 0, tauG = 0;
     int first_start = INT_MAX, first_f = INT_MAX, last_w = 0;
-    int ecount = 0;
+    int ecount = 0, ecount0 = 0;             // events committed / restored from a checkpoint
     uint32_t head = 0, nxt = 0;
     int cpos = 0;
     uint32_t chead = NO_CHAN, cnext = NO_CHAN;
@@ -186,16 +206,15 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
         return __ldg(&p.chorders[((size_t)cand * p.G + chan_i) * p.chan_stride + q]);
     };
 
-    // Ledger window: ring of K (time, delta) points sorted by time, all >= the fold line.
+    // Ledger window: the stage's merged breakpoints at or after the fold line, sorted by time, each
+    // holding the usage AFTER it; slots [ws, we) of a 2K array, compacted when the end is reached.
+    // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
     auto win_fold = [&](int line) {
-        while (wn > 0 && (int)wt[wh] < line) {
-            int t = (int)wt[wh];
-            do {
-                base += wd[wh];
-                wh = (wh + 1) & KM;
-                --wn;
-            } while (wn > 0 && (int)wt[wh] == t);
-            peak = base > peak ? base : peak;
+        while (ws < we && (int)wt[ws] < line) {
+            V u = wu[ws];
+            peak = u > peak ? u : peak;
+            base = u;
+            ++ws;
         }
     };
     // Called before sfree / cfree / n_unrel reflect the event being committed: the fold line is
@@ -205,36 +224,31 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
         win_fold(n_unrel > 0 ? min(sfree, cfree) : sfree);
         top += d;
         rF = rG = V(-1);                               // the ledger changed: drop cached answers
-        if (wn == K) { ovf = true; return; }
-        int k = wn;
-        while (k > 0) {
-            int src = (wh + k - 1) & KM;
-            if ((int)wt[src] <= t) break;
-            int dst = (wh + k) & KM;
-            wt[dst] = wt[src];
-            wd[dst] = wd[src];
-            --k;
+        int k = we - 1;
+        while (k >= ws && (int)wt[k] > t) --k;         // last breakpoint at or before t
+        if (k >= ws && (int)wt[k] == t) {              // same time: merge into that breakpoint
+            for (int q = k; q < we; ++q) wu[q] += d;
+            return;
         }
-        int dst = (wh + k) & KM;
-        wt[dst] = (uint32_t)t;
-        wd[dst] = d;
-        ++wn;
+        if (we - ws == K) { ovf = true; return; }
+        if (we == 2 * K) {                             // compact to the front
+            for (int q = ws; q < we; ++q) { wt[q - ws] = wt[q]; wu[q - ws] = wu[q]; }
+            k -= ws;
+            we -= ws;
+            ws = 0;
+        }
+        for (int q = we - 1; q > k; --q) { wt[q + 1] = wt[q]; wu[q + 1] = wu[q] + d; }
+        wt[k + 1] = (uint32_t)t;
+        wu[k + 1] = (k >= ws ? wu[k] : base) + d;
+        ++we;
     };
-    // earliest_fit core: first breakpoint after the last one whose usage exceeds R.
+    // earliest_fit core: first breakpoint after the last one whose usage exceeds R (SURVEY.md A.3).
     auto win_tau = [&](V R) -> int {
-        if (R < 0) return TAU_NONE;
-        V u = top;
-        if (u > R) return TAU_NONE;
-        int k = wn - 1;
-        while (k >= 0) {
-            int t = (int)wt[(wh + k) & KM];
-            do {
-                u -= wd[(wh + k) & KM];
-                --k;
-            } while (k >= 0 && (int)wt[(wh + k) & KM] == t);
-            if (u > R) return t;
-        }
-        return TAU_ANY;
+        if (R < 0 || top > R) return TAU_NONE;
+        int k = we - 1;
+        while (k >= ws && !(wu[k] > R)) --k;
+        if (k >= ws) return (int)wt[k + 1];
+        return base > R && ws < we ? (int)wt[ws] : TAU_ANY;
     };
     auto tau_F = [&](V R) -> int {
         if (R != rF) { tauF = win_tau(R); rF = R; }
@@ -330,7 +344,7 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
 
     // Lane 0 publishes a candidate's outcome (search rounds may pass no arrays).
     auto put_result = [&](uint32_t flag, long long span, uint32_t blocked_mask) {
-        if (p.events_total && ecount) atomicAdd(p.events_total, (unsigned long long)ecount);
+        if (p.events_total && ecount > ecount0) atomicAdd(p.events_total, (unsigned long long)(ecount - ecount0));
         if (p.flags) p.flags[cand] = flag;
         if (p.makespan) p.makespan[cand] = span;
         if (p.bubble)
@@ -338,6 +352,23 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
                                       : __longlong_as_double(0x7ff8000000000000LL);
         if (p.blocked) p.blocked[cand] = blocked_mask;
     };
+
+    // Checkpoint = the candidate's shared state + every lane's scalar state, before step c*C.
+    auto save_regs = [&](uint32_t *rg) {
+        rg[0] = pos; rg[1] = sfree; rg[2] = cfree; rg[3] = ws; rg[4] = we; rg[5] = n_poff; rg[6] = n_prel;
+        rg[7] = n_unrel; rg[8] = first_start; rg[9] = first_f; rg[10] = last_w;
+        *reinterpret_cast<long long *>(rg + 12) = (long long)base;
+        *reinterpret_cast<long long *>(rg + 14) = (long long)top;
+        *reinterpret_cast<long long *>(rg + 16) = (long long)peak;
+    };
+    auto load_regs = [&](const uint32_t *rg) {
+        pos = rg[0]; sfree = rg[1]; cfree = rg[2]; ws = rg[3]; we = rg[4]; n_poff = rg[5]; n_prel = rg[6];
+        n_unrel = rg[7]; first_start = rg[8]; first_f = rg[9]; last_w = rg[10];
+        base = (V)*reinterpret_cast<const long long *>(rg + 12);
+        top = (V)*reinterpret_cast<const long long *>(rg + 14);
+        peak = (V)*reinterpret_cast<const long long *>(rg + 16);
+    };
+    const int n_ck = (p.ck && !REC) ? p.base_info[0] : 0;
 
     const long long n_items = p.work_list ? (long long)*p.work_count : p.N;
     for (long long item = slot; item < n_items; item += nslots) {
@@ -351,9 +382,10 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
         }
         __syncwarp();
         bool bad = false;
-        n_unrel = 0;
-        if (has_stage) {
+        // this stage's offload bits of the candidate, re-based to [MW] words; returns their count
+        auto build_mask = [&](bool check) -> int {
             const int mwords = (P * m + 31) / 32;
+            int n = 0;
             for (int w = 0; w < MW; ++w) {
                 // bits [i*m + 32w, i*m + 32w + 32) of the packed candidate mask
                 const int gb = i * m + w * 32, q = gb >> 5, sh = gb & 31;
@@ -367,11 +399,17 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
                 if (nb < 32) bits &= (1u << nb) - 1u;
                 if (MOVES && mv.type == MOVE_TOGGLE && mv.stage == i && (mv.mb >> 5) == w) bits ^= 1u << (mv.mb & 31);
                 offm_i[w] = bits;
-                n_unrel += __popc(bits);
+                n += __popc(bits);
                 // an offload bit on a non-offloadable op is malformed (KeyError in the reference)
-                for (uint32_t t = bits; t; t &= t - 1)
-                    if (!(val_of(w * 32 + __ffs(t) - 1, 3) > 0)) bad = true;
+                if (check)
+                    for (uint32_t t = bits; t; t &= t - 1)
+                        if (!(val_of(w * 32 + __ffs(t) - 1, 3) > 0)) bad = true;
             }
+            return n;
+        };
+        int cand_unrel = 0;
+        if (has_stage) {
+            cand_unrel = build_mask(true);
             if (!MOVES) {
                 // the stage order must be a permutation of the stage's 3m ops
                 for (int q = 0; q < L; ++q) {
@@ -391,19 +429,100 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
             __syncwarp();
             continue;
         }
-        pos = 0; sfree = 0; cfree = 0; ovf = false;
-        base = top = peak = 0; wh = wn = 0;
-        n_poff = n_prel = 0;
+        // ---- prefix sharing: the first step whose inputs differ from the recorded base ----
+        uint32_t div = 0u;
+        if (n_ck > 0) {
+            uint32_t d = NEVER;
+            if (has_stage) {
+                auto after = [&](int q) -> uint32_t {   // first step at which stage i's head is position q
+                    if (q == 0) return 0u;
+                    uint32_t c = p.cstep[i * L + q - 1];
+                    return c == NEVER ? NEVER : c + 1u;
+                };
+                if (MOVES) {
+                    if (mv.stage == i) {
+                        if (mv.type == MOVE_SHIFT) d = after(min(mv.a, mv.b));
+                        else if (mv.type == MOVE_TOGGLE) d = p.fstep[i * m + mv.mb];
+                    }
+                } else {
+                    const uint16_t *row = p.orders + ((size_t)cand * P + i) * p.stride;
+                    const uint16_t *brow = p.base_orders + (size_t)i * p.stride;
+                    int q = 0;
+                    while (q < L && row[q] == brow[q]) ++q;
+                    if (q < L) d = after(q);
+                    const int mwords = (P * m + 31) / 32;
+                    for (int w = 0; w < MW; ++w) {
+                        const int gb = i * m + w * 32, qq = gb >> 5, sh = gb & 31;
+                        uint32_t bb = (qq < mwords ? p.base_mask[qq] : 0u) >> sh;
+                        if (sh && qq + 1 < mwords) bb |= p.base_mask[qq + 1] << (32 - sh);
+                        for (uint32_t x = (offm_i[w] ^ bb) & (m - w * 32 < 32 ? (1u << (m - w * 32)) - 1u : ~0u); x; x &= x - 1)
+                            d = min(d, p.fstep[i * m + w * 32 + __ffs(x) - 1]);
+                    }
+                }
+            }
+            div = __reduce_min_sync(0xffffffffu, d);
+            if (div == NEVER) {
+                // identical to the base up to its end: its outcome is this candidate's
+                if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = p.base_res[2 + i];
+                if (lane == 0) {
+                    ecount = ecount0 = 0;
+                    const long long span = p.base_res[0];
+                    put_result((uint32_t)p.base_info[1], span, (uint32_t)p.base_info[3]);
+                    if (MOVES && p.best_key && span >= 0) {
+                        long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
+                        if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+        }
+        const int ck_idx = n_ck > 0 ? min((int)(div / (uint32_t)p.ck_interval), n_ck - 1) : 0;
+        if (ck_idx > 0) {
+            const uint32_t *src = p.ck + (size_t)ck_idx * p.ck_words;
+            const int cw = p.cand_words;
+            for (int k = lane; k < cw; k += 32) cb[k] = src[k];
+            load_regs(src + cw + lane * CK_REGW);
+            __syncwarp();
+            if (has_stage) {
+                // this candidate's offload bits: any difference lies on an F the base has not
+                // committed yet, so only the outstanding-transfer count moves
+                int nb = 0;
+                for (int w = 0; w < MW; ++w) nb += __popc(offm_i[w]);
+                n_unrel += cand_unrel - nb;
+                build_mask(false);
+            }
+            ecount = ck_idx * p.ck_interval;
+            ecount0 = ecount;
+        } else {
+            ecount0 = 0;
+            pos = 0; sfree = 0; cfree = 0;
+            base = top = peak = 0; ws = we = 0;
+            n_poff = n_prel = 0;
+            n_unrel = cand_unrel;
+            first_start = INT_MAX; first_f = INT_MAX; last_w = 0; ecount = 0;
+        }
+        ovf = false;
         rF = rG = V(-1);
-        first_start = INT_MAX; first_f = INT_MAX; last_w = 0; ecount = 0;
-        head = fetch(0); nxt = fetch(1);
+        head = fetch(pos); nxt = fetch(pos + 1);
         cpos = 0; chead = fetch_chan(0); cnext = fetch_chan(1);
         cdirty = tdirty = has_stage;
         ckh = ckl = tkh = tkl = KEY_NONE;
         __syncwarp();
 
         // ================= simulate: one committed event per iteration ===================
+        bool ck_full = false;
         for (;;) {
+            if (REC && (ecount & (p.ck_interval - 1)) == 0) {
+                const int c = ecount / p.ck_interval;
+                if (c < p.ck_max) {
+                    uint32_t *dst = p.ck + (size_t)c * p.ck_words;
+                    for (int q = lane; q < p.cand_words; q += 32) dst[q] = cb[q];
+                    save_regs(dst + p.cand_words + lane * CK_REGW);
+                } else {
+                    ck_full = true;
+                }
+            }
             if (cdirty) { compute_key(); cdirty = false; }
             if (tdirty) { transfer_key(); tdirty = false; }
             uint32_t kh = ckh, kl = ckl;
@@ -420,6 +539,10 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
             if (p.tcode && i == w) {
                 p.tcode[(size_t)cand * p.tstride + ecount] = ml;
                 p.tstart[(size_t)cand * p.tstride + ecount] = t;
+            }
+            if (REC && rank == RANK_COMPUTE && i == w) {
+                p.cstep[i * L + pos] = (uint32_t)ecount;
+                if (k == KIND_F) p.fstep[i * m + j] = (uint32_t)ecount;
             }
             ++ecount;
             if (rank == RANK_COMPUTE) {
@@ -484,7 +607,27 @@ __global__ void __launch_bounds__(128) eval_kernel(const EvalParams p) {
 
         // ================= finished or deadlocked =========================================
         const unsigned rem = __ballot_sync(0xffffffffu, has_stage && pos < L);
-        if (__any_sync(0xffffffffu, ovf)) {
+        if (REC) {
+            const bool unusable = __any_sync(0xffffffffu, ovf || ck_full);
+            long long span = -1;
+            if (!unusable && rem == 0u) {
+                win_fold(INT_MAX);
+                int hi = p.post ? (has_stage ? last_w - first_f : 0) : (has_stage ? sfree : 0);
+                int lo = p.post ? 0 : (has_stage ? first_start : INT_MAX);
+                span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, lo);
+            }
+            if (has_stage) p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
+            if (lane == 0) {
+                p.base_info[0] = unusable ? -1 : ecount / p.ck_interval + 1;
+                p.base_info[1] = (int)(rem == 0u ? FLAG_FEASIBLE : FLAG_DEADLOCK);
+                p.base_info[2] = ecount;
+                p.base_info[3] = (int)rem;
+                p.base_res[0] = span;
+                double b = span > 0 ? 1.0 - (double)p.busy / ((double)P * (double)span)
+                                    : __longlong_as_double(0x7ff8000000000000LL);
+                p.base_res[1] = __double_as_longlong(b);
+            }
+        } else if (__any_sync(0xffffffffu, ovf)) {
             if (lane == 0 && p.ovf_list) {
                 int at = atomicAdd(p.ovf_count, 1);
                 p.ovf_list[at] = (int32_t)cand;

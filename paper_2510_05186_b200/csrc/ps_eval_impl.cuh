@@ -4,9 +4,9 @@
 
 namespace ps {
 
-template <typename V, bool MOVES, bool GSTATE>
+template <typename V, bool MOVES, bool GSTATE, bool REC>
 static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t stream) {
-    auto fn = eval_kernel<V, MOVES, GSTATE>;
+    auto fn = eval_kernel<V, MOVES, GSTATE, REC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
     if (e != cudaSuccess) return e;
     fn<<<cfg.grid, cfg.block, cfg.smem, stream>>>(p);
@@ -15,16 +15,17 @@ static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t s
 
 template <typename V, bool MOVES, bool GSTATE>
 static cudaError_t occ_one(int block, size_t smem, int *n) {
-    auto fn = eval_kernel<V, MOVES, GSTATE>;
+    auto fn = eval_kernel<V, MOVES, GSTATE, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, fn, block, smem);
 }
 
 template <typename V>
-cudaError_t eval_launch(bool moves, bool gstate, const EvalParams &p, LaunchCfg cfg, cudaStream_t s) {
-    if (moves) return gstate ? launch_one<V, true, true>(p, cfg, s) : launch_one<V, true, false>(p, cfg, s);
-    return gstate ? launch_one<V, false, true>(p, cfg, s) : launch_one<V, false, false>(p, cfg, s);
+cudaError_t eval_launch(bool moves, bool gstate, bool record, const EvalParams &p, LaunchCfg cfg, cudaStream_t s) {
+    if (record) return launch_one<V, false, false, true>(p, cfg, s);
+    if (moves) return gstate ? launch_one<V, true, true, false>(p, cfg, s) : launch_one<V, true, false, false>(p, cfg, s);
+    return gstate ? launch_one<V, false, true, false>(p, cfg, s) : launch_one<V, false, false, false>(p, cfg, s);
 }
 
 template <typename V>

@@ -10,9 +10,10 @@ struct LaunchCfg {
     size_t smem;
 };
 
-// Variant = (ledger value type V, move-encoded candidates, state in global memory).
+// Variant = (ledger value type V, move-encoded candidates, state in global memory, base recording).
 template <typename V>
-cudaError_t eval_launch(bool moves, bool gstate, const EvalParams &p, LaunchCfg cfg, cudaStream_t stream);
+cudaError_t eval_launch(bool moves, bool gstate, bool record, const EvalParams &p, LaunchCfg cfg,
+                        cudaStream_t stream);
 template <typename V>
 cudaError_t eval_occupancy(bool moves, bool gstate, int block, size_t smem, int *blocks_per_sm);
 

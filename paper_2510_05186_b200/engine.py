@@ -94,25 +94,28 @@ class DeviceInstance:
             trace_code=torch.empty((n, E), dtype=torch.int32, device=dev) if trace else None,
             trace_start=torch.empty((n, E), dtype=torch.int32, device=dev) if trace else None)
 
-    def _batch_structs(self, n, orders, masks, chans, res: EvalResult):
+    def _batch_structs(self, n, orders, masks, chans, res: EvalResult, base=None):
         cb = N.CandBatch(n, _ptr(orders), _ptr(masks), _ptr(chans),
-                         int(chans.shape[-1]) if chans is not None else 0)
+                         int(chans.shape[-1]) if chans is not None else 0,
+                         base.handle if base is not None else None)
         rb = N.ResultBatch(_ptr(res.makespan), _ptr(res.bubble), _ptr(res.peak), _ptr(res.flags),
                            _ptr(res.blocked), _ptr(res.trace_code), _ptr(res.trace_start),
                            int(res.trace_code.shape[-1]) if res.trace_code is not None else 0)
         return cb, rb
 
     def evaluate(self, orders, masks, chans=None, out: EvalResult | None = None, peak=True,
-                 trace=False, stream=None) -> EvalResult:
-        """Device tensors in, device tensors out; asynchronous on `stream`."""
+                 trace=False, stream=None, base: "Base | None" = None) -> EvalResult:
+        """Device tensors in, device tensors out; asynchronous on `stream`.  With a recorded
+        `base`, candidates resume from its last checkpoint before they first differ from it."""
         n = int(orders.shape[0])
         res = out if out is not None else self.alloc_results(n, peak=peak, trace=trace)
-        cb, rb = self._batch_structs(n, orders, masks, chans, res)
+        cb, rb = self._batch_structs(n, orders, masks, chans, res, base)
         N.check(self.lib.ps_eval_batch(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
         return res
 
     def evaluate_host(self, orders: np.ndarray, masks: np.ndarray, chans=None, peak=True,
-                      trace=False, out: EvalResult | None = None, stream=None) -> EvalResult:
+                      trace=False, out: EvalResult | None = None, stream=None,
+                      base: "Base | None" = None) -> EvalResult:
         """Host (ideally pinned) numpy buffers in and out: copies inside the call."""
         n = int(orders.shape[0])
         if out is None:
@@ -122,9 +125,25 @@ class DeviceInstance:
                              np.empty((n, E), np.int32) if trace else None,
                              np.empty((n, E), np.int32) if trace else None)
         cb, rb = self._batch_structs(n, np.ascontiguousarray(orders), np.ascontiguousarray(masks),
-                                     None if chans is None else np.ascontiguousarray(chans), out)
+                                     None if chans is None else np.ascontiguousarray(chans), out, base)
         N.check(self.lib.ps_eval_batch_host(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
         return out
+
+
+class Base:
+    """A recorded base candidate (``ps_base``) for prefix sharing."""
+
+    def __init__(self, di: DeviceInstance):
+        self.di = di
+        h = C.c_void_p()
+        N.check(di.lib.ps_base_create(di.handle, C.byref(h)))
+        self.handle = h
+        self._finalizer = weakref.finalize(self, di.lib.ps_base_destroy, h)
+
+    def record(self, orders, mask, stream=None):
+        """orders: device int16 [P, stride]; mask: device int32 [mask_words]."""
+        N.check(self.di.lib.ps_base_record(self.handle, C.c_void_p(orders.data_ptr()),
+                                           C.c_void_p(mask.data_ptr()), self.di._stream(stream)))
 
 
 _CACHE: dict = {}

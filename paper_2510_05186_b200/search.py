@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .engine import device_instance
+from .engine import Base, device_instance
 from .packing import decode_mask, decode_orders, encode_candidate
 
 
@@ -35,6 +35,7 @@ class SearchConfig:
     neighbours: int = 65536          # per round, all ranks together
     shift_permille: int = 700        # SHIFT moves; the rest toggle offload bits
     max_shift: int = 4
+    share_prefix: bool = True        # resume neighbours from checkpoints of the incumbent
 
 
 @dataclass
@@ -115,6 +116,9 @@ class LocalSearch:
             raise ValueError("the incumbent structure is not feasible")
         self.makespan = int(res.makespan[0].item())
         self.initial_makespan = self.makespan
+        self.base = Base(self.di) if config.share_prefix else None
+        if self.base is not None:
+            self.base.record(self.inc_orders, self.inc_mask)
         self.round = 0
         self.evaluated = 0
         self.improvements = []
@@ -127,7 +131,8 @@ class LocalSearch:
         """Enqueue one round's generate + evaluate + argmin (no host sync)."""
         self.best_key.fill_(N.BEST_NONE)
         desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round,
-                            self.first, self.count, self.moves)
+                            self.first, self.count, self.moves, None,
+                            self.base.handle if self.base is not None else None)
         N.check(self.lib.ps_search_round(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
                                          C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None,
                                          self._stream()))
@@ -146,6 +151,8 @@ class LocalSearch:
         N.check(self.lib.ps_apply_move(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
                                        C.c_void_p(self.inc_mask.data_ptr()), C.byref(self.moves),
                                        r, idx, self._stream()))
+        if self.base is not None:
+            self.base.record(self.inc_orders, self.inc_mask)
         self.makespan = span
         self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
         return True

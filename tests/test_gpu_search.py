@@ -116,3 +116,52 @@ def test_generators_match_reference_outputs(cuda_ok):
         s, name = best_feasible(inst)
         assert name == row["best_feasible"]["name"]
         assert makespan(s, inst) == row["best_feasible"]["makespan"]
+
+
+def _eval_both(di, orders, masks, base):
+    r0 = di.evaluate(orders, masks, peak=True)
+    r1 = di.evaluate(orders, masks, peak=True, base=base)
+    import torch
+    torch.cuda.synchronize()
+    for f in ("flags", "makespan", "peak", "blocked"):
+        a, b = getattr(r0, f).cpu().numpy(), getattr(r1, f).cpu().numpy()
+        assert (a == b).all(), f
+    ok = (r0.flags.cpu().numpy() & 1) == 1
+    assert (r0.bubble.cpu().numpy()[ok] == r1.bubble.cpu().numpy()[ok]).all()
+    return r0
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_prefix_sharing_is_exact(cuda_ok, cfg):
+    """Evaluations resumed from the recorded incumbent's checkpoints equal full simulations."""
+    import ctypes as C
+    import torch
+    from paper_2510_05186_b200 import _native as N
+    from paper_2510_05186_b200.engine import Base
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    n = 1024
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT, share_prefix=True))
+    # materialised neighbours, with and without the base
+    o, mk = ls.materialize(0, n, 0)
+    r = _eval_both(ls.di, o, mk, ls.base)
+    # search-round makespans, with and without the base
+    ms = []
+    for base in (None, ls.base):
+        out = torch.empty(n, dtype=torch.int64, device="cuda")
+        ls.best_key.fill_(N.BEST_NONE)
+        desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), 0, 0, n, ls.moves, None,
+                            base.handle if base is not None else None)
+        N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
+                                       C.c_void_p(out.data_ptr()), ls._stream()))
+        torch.cuda.synchronize()
+        ms.append((out.cpu().numpy(), int(ls.best_key.item())))
+    assert (ms[0][0] == ms[1][0]).all() and ms[0][1] == ms[1][1]
+    assert (ms[0][0] == r.makespan.cpu().numpy()).all()
+    # an unrelated (deadlocking) base: still exact
+    bad = Base(ls.di)
+    o2 = o[1:2].clone()
+    row = o2[0, 0].clone()
+    o2[0, 0, :2] = torch.flip(row[:2], [0])
+    bad.record(o2[0], mk[1])
+    _eval_both(ls.di, o, mk, bad)

@@ -24,8 +24,8 @@ def main():
     ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=1, neighbours=n))
     stream = torch.cuda.current_stream()
     od, md = ls.materialize(0, n)
-    grid = [(1, win, warps) for win in (8, 16, 32) for warps in (4, 2, 1)]
-    for segs, win, warps in grid:
+    grid = [(1, win, warps) for win in [int(x) for x in os.environ.get('KEXP_WINDOWS', '16').split(',')] for warps in (4,)]
+    for (segs, win, warps), share in [(g, sh) for g in grid for sh in (False, True)]:
         os.environ["PS_SEGS_PER_WARP"] = str(segs)
         os.environ["PS_WINDOW"] = str(win)
         os.environ["PS_WARPS_PER_BLOCK"] = str(warps)
@@ -38,16 +38,17 @@ def main():
                 e0.record()
                 if mode == "search":
                     ls.best_key.fill_(N.BEST_NONE)
-                    desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), 0, 0, n, ls.moves, None)
+                    desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), 0, 0, n, ls.moves, None,
+                                        ls.base.handle if (share and ls.base is not None) else None)
                     N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
                                                    None, C.c_void_p(stream.cuda_stream)))
                 else:
-                    ls.di.evaluate(od, md, peak=True)
+                    ls.di.evaluate(od, md, peak=True, base=ls.base if share else None)
                 e1.record()
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             res[mode] = min(ts)
-        print(json.dumps({"config": cfg_id, "segs": segs, "window": win, "warps": warps,
+        print(json.dumps({"share": share, "lib": os.path.basename(os.environ.get("PS_LIBRARY", "default")), "config": cfg_id, "segs": segs, "window": win, "warps": warps,
                           "search_ms": round(res["search"], 3), "mat_ms": round(res["materialized"], 3),
                           "search_cps": round(n / res["search"] * 1e3), "mat_cps": round(n / res["materialized"] * 1e3)}),
               flush=True)
