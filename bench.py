@@ -244,6 +244,8 @@ def main():
         dist.barrier()
     step_ms = [evs[k][0].elapsed_time(evs[k][3]) for k in range(K)]
     kern_ms = [evs[k][1].elapsed_time(evs[k][2]) for k in range(K)]
+    print(json.dumps({"diag_step_ms": [round(x, 2) for x in step_ms], "diag_kern_ms": [round(x, 2) for x in kern_ms]}),
+          file=sys.stderr, flush=True)
     total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)

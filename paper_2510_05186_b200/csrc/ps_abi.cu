@@ -134,11 +134,14 @@ int env_int(const char *name, int dflt) {
 // Shared-memory plan for the main pass: one candidate per warp, ledger window K (12 by default, or
 // the whole 5m ledger when that is smaller and cannot overflow), as many warps per block as fit;
 // state moves to global memory only when a single warp's state does not fit.
-int window_size(const ps_instance *I) { return std::min(std::max(4, env_int("PS_WINDOW", 12)), 5 * I->m); }
+int window_size(const ps_instance *I) { return std::min(std::max(4, env_int("PS_WINDOW", 16)), 5 * I->m); }
 
-int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
-    pl->K = window_size(I);
-    pl->cand_words = words_per_candidate(I, pl->K);
+// One evaluation pass with ledger window K: one candidate per warp, as many warps per block as fit
+// in shared memory; the state moves to global memory only when a single warp's does not fit.
+// `N` bounds the grid (a worklist pass may receive fewer candidates, never more).
+int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl) {
+    pl->K = K;
+    pl->cand_words = words_per_candidate(I, K);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
     pl->warps = 4;
@@ -153,7 +156,11 @@ int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
             break;
         }
     }
-    if (pl->gstate) pl->cfg.smem = (size_t)pl->inc_words * 4;
+    if (pl->gstate) {
+        // global-memory state: one warp per block and a bounded grid keep the scratch small
+        pl->warps = 1;
+        pl->cfg.smem = (size_t)pl->inc_words * 4;
+    }
     if (pl->cfg.smem > (size_t)I->max_smem_optin)
         return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
     pl->cfg.block = 32 * pl->warps;
@@ -162,22 +169,9 @@ int plan_main(const ps_instance *I, bool moves, int64_t N, Plan *pl) {
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     if (per_sm < 1) per_sm = 1;
     int64_t want = (N + pl->warps - 1) / pl->warps;
-    pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * I->num_sms));
+    int64_t cap = pl->gstate ? 2 * (int64_t)I->num_sms : (int64_t)per_sm * I->num_sms;
+    pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
     pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * pl->warps * pl->cand_words * 4 : 0;
-    return PS_OK;
-}
-
-// Overflow pass: window of 5m points per stage (the whole ledger), state in global memory.
-int plan_retry(const ps_instance *I, bool moves, Plan *pl) {
-    pl->K = 5 * I->m;
-    pl->cand_words = words_per_candidate(I, pl->K);
-    pl->inc_words = incumbent_words(I, moves);
-    pl->gstate = true;
-    pl->warps = 1;
-    pl->cfg.block = 32;
-    pl->cfg.smem = (size_t)pl->inc_words * 4;
-    pl->cfg.grid = I->num_sms;
-    pl->scratch_bytes = (size_t)pl->cfg.grid * pl->cand_words * 4;
     return PS_OK;
 }
 
@@ -198,53 +192,50 @@ void attach_base(const ps_base *B, EvalParams *p) {
     p->base_mask = B->mask;
     p->ck_interval = B->ck_interval;
     p->ck_words = B->ck_words;
+    p->ck_kc = B->K;
     p->ck_max = B->ck_max;
 }
 
-// Main pass + overflow pass on one stream; all scratch is stream-ordered.
+// Evaluation cascade on one stream, all scratch stream-ordered: a pass with the default window
+// K1, then a shared-memory pass with a 4x wider window over the candidates whose ledger did not
+// fit, then a pass with the whole 5m-point ledger (cannot overflow) over what is left.  Every pass
+// reads its worklist from device memory: no host round trip.
 int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr) {
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
-    Plan main_pl, retry_pl;
-    int rc = plan_main(I, moves, p.N, &main_pl);
-    if (rc) return rc;
-    // a base is usable when the main pass runs in shared memory with the window it was recorded with
-    if (B && B->inst == I && !main_pl.gstate && B->K == main_pl.K && p.chorders == nullptr && p.tcode == nullptr)
-        attach_base(B, &p);
-    plan_retry(I, moves, &retry_pl);
-    int32_t *ovf = nullptr;
-    uint32_t *scratch = nullptr, *scratch2 = nullptr;
-    PS_CUDA(cudaMallocAsync((void **)&ovf, (size_t)(p.N + 1) * sizeof(int32_t), s));
-    PS_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int32_t), s));
-    if (main_pl.scratch_bytes) PS_CUDA(cudaMallocAsync((void **)&scratch, main_pl.scratch_bytes, s));
-    PS_CUDA(cudaMallocAsync((void **)&scratch2, retry_pl.scratch_bytes, s));
-
-    p.ovf_count = ovf;
-    p.ovf_list = ovf + 1;
-    p.work_list = nullptr;
-    p.work_count = nullptr;
-    p.K = main_pl.K;
-    p.cand_words = main_pl.cand_words;
-    p.inc_words = main_pl.inc_words;
-    p.gstate = scratch;
-    cudaError_t e = launch(I->v64, moves, main_pl.gstate, p, main_pl.cfg, s);
-    if (e != cudaSuccess) return cuda_fail(e, "evaluator launch");
-
-    EvalParams q = p;
-    q.ck = nullptr;           // the overflow pass re-simulates from scratch with the full ledger
-    q.work_list = ovf + 1;
-    q.work_count = ovf;
-    q.ovf_list = nullptr;     // the full-ledger window cannot overflow
-    q.ovf_count = nullptr;
-    q.K = retry_pl.K;
-    q.cand_words = retry_pl.cand_words;
-    q.inc_words = retry_pl.inc_words;
-    q.gstate = scratch2;
-    e = launch(I->v64, moves, true, q, retry_pl.cfg, s);
-    if (e != cudaSuccess) return cuda_fail(e, "evaluator overflow launch");
-    if (scratch) PS_CUDA(cudaFreeAsync(scratch, s));
-    PS_CUDA(cudaFreeAsync(scratch2, s));
-    PS_CUDA(cudaFreeAsync(ovf, s));
+    const int full = 5 * I->m;
+    int Ks[3] = {window_size(I), std::min(full, 4 * window_size(I)), full};
+    int npass = 1;
+    if (Ks[0] < full) npass = Ks[1] < full ? 3 : 2;
+    if (B && B->inst == I && p.chorders == nullptr && p.tcode == nullptr) attach_base(B, &p);
+    // worklists, one per handoff between passes: [count][N candidate indices]
+    int32_t *lists = nullptr;
+    const size_t list_words = (size_t)p.N + 1;
+    PS_CUDA(cudaMallocAsync((void **)&lists, 2 * list_words * sizeof(int32_t), s));
+    PS_CUDA(cudaMemsetAsync(lists, 0, sizeof(int32_t), s));
+    PS_CUDA(cudaMemsetAsync(lists + list_words, 0, sizeof(int32_t), s));
+    for (int k = 0; k < npass; ++k) {
+        Plan pl;
+        int rc = plan_pass(I, moves, Ks[k], p.N, &pl);
+        if (rc) return rc;
+        EvalParams q = p;
+        q.K = pl.K;
+        q.cand_words = pl.cand_words;
+        q.inc_words = pl.inc_words;
+        int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : nullptr;       // handoff k-1
+        int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
+        q.work_count = in;
+        q.work_list = in ? in + 1 : nullptr;
+        q.ovf_count = out;
+        q.ovf_list = out ? out + 1 : nullptr;
+        uint32_t *scratch = nullptr;
+        if (pl.scratch_bytes) PS_CUDA(cudaMallocAsync((void **)&scratch, pl.scratch_bytes, s));
+        q.gstate = scratch;
+        cudaError_t e = launch(I->v64, moves, pl.gstate, q, pl.cfg, s);
+        if (e != cudaSuccess) return cuda_fail(e, k ? "evaluator overflow pass" : "evaluator launch");
+        if (scratch) PS_CUDA(cudaFreeAsync(scratch, s));
+    }
+    PS_CUDA(cudaFreeAsync(lists, s));
     return PS_OK;
 }
 
@@ -496,19 +487,25 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     ps_base *B = new (std::nothrow) ps_base();
     if (!B) return fail(PS_ERR_NOMEM, "host allocation");
     B->inst = I;
-    B->K = window_size(I);
+    B->K = std::min(5 * I->m, 128);                 // recording window (checkpoints store it compactly)
     B->cand_words = words_per_candidate(I, B->K);
-    B->ck_words = B->cand_words + 32 * CK_REGW;
+    {
+        const int vw = I->v64 ? 2 : 1;
+        const int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
+        const int ck_t = (nz + 1) & ~1;
+        const int ck_u = (ck_t + I->P * B->K + 1) & ~1;
+        B->ck_words = ck_u + I->P * B->K * vw + 32 * CK_REGW;
+    }
     B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 32))));
     B->ck_max = 5 * I->P * I->m / B->ck_interval + 2;
     cudaError_t e = cudaMalloc((void **)&B->ck, (size_t)B->ck_max * B->ck_words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->cstep, (size_t)I->P * I->L * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->fstep, (size_t)I->P * I->m * 4);
-    if (e == cudaSuccess) e = cudaMalloc((void **)&B->info, 4 * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->info, 8 * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->res, (size_t)(2 + I->P) * sizeof(int64_t));
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->orders, (size_t)I->P * I->stride * 2);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->mask, (size_t)I->mask_words * 4);
-    if (e == cudaSuccess) e = cudaMemset(B->info, 0xFF, 4 * sizeof(int32_t));   // -1: nothing recorded
+    if (e == cudaSuccess) e = cudaMemset(B->info, 0xFF, 8 * sizeof(int32_t));   // -1: nothing recorded
     if (e != cudaSuccess) {
         ps_base_destroy(B);
         return fail(PS_ERR_NOMEM, "base workspace: %s", cudaGetErrorString(e));

@@ -79,12 +79,13 @@ struct EvalParams {
     uint32_t *gstate;        // GSTATE scratch
     // prefix sharing against a recorded base candidate
     int ck_interval;         // steps between checkpoints (power of two)
-    int ck_words;            // words per checkpoint: cand_words + 32 * CK_REGW
+    int ck_words;            // words per checkpoint (layout independent of the window K, see below)
+    int ck_kc;               // checkpoint window capacity per stage (the base was recorded with it)
     int ck_max;              // checkpoint capacity
     uint32_t *ck;            // [ck_max][ck_words]; NULL = no base
     uint32_t *cstep;         // [P][L] step at which the base commits stage i's q-th op (~0 = never)
     uint32_t *fstep;         // [P][m] step at which the base commits F(i, j)
-    int32_t *base_info;      // [0] checkpoints (-1 unusable) [1] flags [2] events [3] blocked
+    int32_t *base_info;      // [0] checkpoints (-1 unusable) [1] flags [2] events [3] blocked [4] max window
     int64_t *base_res;       // [0] makespan [1] bubble bits [2 .. 2+P) peaks
     const uint16_t *base_orders;   // [P][stride] (materialised candidates)
     const uint32_t *base_mask;     // [mask_words]
@@ -353,7 +354,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (p.blocked) p.blocked[cand] = blocked_mask;
     };
 
-    // Checkpoint = the candidate's shared state + every lane's scalar state, before step c*C.
+    // Checkpoint (state before step c*C), independent of the evaluating pass's window K:
+    //   [0, nz)               A, X, offm, poff, prel
+    //   [ck_t, ck_t + P*KC)   each stage's live breakpoint times, compacted to slot 0
+    //   [ck_u, ck_u + P*KC*VW) their usages
+    //   [ck_r, ck_r + 32*CK_REGW) every lane's scalars (window as ws = 0, we = count)
+    const int ck_t = (nz + 1) & ~1;
+    const int ck_u = (ck_t + P * p.ck_kc + 1) & ~1;
+    const int ck_r = ck_u + P * p.ck_kc * VW;
     auto save_regs = [&](uint32_t *rg) {
         rg[0] = pos; rg[1] = sfree; rg[2] = cfree; rg[3] = ws; rg[4] = we; rg[5] = n_poff; rg[6] = n_prel;
         rg[7] = n_unrel; rg[8] = first_start; rg[9] = first_f; rg[10] = last_w;
@@ -480,9 +488,22 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         const int ck_idx = n_ck > 0 ? min((int)(div / (uint32_t)p.ck_interval), n_ck - 1) : 0;
         if (ck_idx > 0) {
             const uint32_t *src = p.ck + (size_t)ck_idx * p.ck_words;
-            const int cw = p.cand_words;
-            for (int k = lane; k < cw; k += 32) cb[k] = src[k];
-            load_regs(src + cw + lane * CK_REGW);
+            load_regs(src + ck_r + lane * CK_REGW);
+            if (__any_sync(0xffffffffu, has_stage && we > K)) {
+                // the base's window at this point does not fit this pass: hand over to a wider pass
+                if (lane == 0 && p.ovf_list) {
+                    int at = atomicAdd(p.ovf_count, 1);
+                    p.ovf_list[at] = (int32_t)cand;
+                }
+                __syncwarp();
+                continue;
+            }
+            for (int k = lane; k < nz; k += 32) A[k] = src[k];
+            if (has_stage) {
+                const uint32_t *st = src + ck_t + i * p.ck_kc;
+                const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
+                for (int q = 0; q < we; ++q) { wt[q] = st[q]; wu[q] = su[q]; }
+            }
             __syncwarp();
             if (has_stage) {
                 // this candidate's offload bits: any difference lies on an F the base has not
@@ -512,13 +533,25 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
 
         // ================= simulate: one committed event per iteration ===================
         bool ck_full = false;
+        int max_win = 0;
         for (;;) {
+            if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
             if (REC && (ecount & (p.ck_interval - 1)) == 0) {
                 const int c = ecount / p.ck_interval;
                 if (c < p.ck_max) {
                     uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                    for (int q = lane; q < p.cand_words; q += 32) dst[q] = cb[q];
-                    save_regs(dst + p.cand_words + lane * CK_REGW);
+                    for (int q = lane; q < nz; q += 32) dst[q] = A[q];
+                    if (has_stage) {
+                        uint32_t *st = dst + ck_t + i * p.ck_kc;
+                        V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
+                        for (int q = ws; q < we; ++q) { st[q - ws] = wt[q]; su[q - ws] = wu[q]; }
+                    }
+                    const int ws0 = ws, we0 = we;
+                    we -= ws;
+                    ws = 0;
+                    save_regs(dst + ck_r + lane * CK_REGW);
+                    ws = ws0;
+                    we = we0;
                 } else {
                     ck_full = true;
                 }
@@ -619,6 +652,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             if (has_stage) p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
             if (lane == 0) {
                 p.base_info[0] = unusable ? -1 : ecount / p.ck_interval + 1;
+                p.base_info[4] = max_win;
                 p.base_info[1] = (int)(rem == 0u ? FLAG_FEASIBLE : FLAG_DEADLOCK);
                 p.base_info[2] = ecount;
                 p.base_info[3] = (int)rem;
