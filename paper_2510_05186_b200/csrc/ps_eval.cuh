@@ -136,19 +136,20 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     // ---- this warp's state slot ----------------------------------------------------------
     const long long slot = (long long)blockIdx.x * nwarps + warp;
     const long long nslots = (long long)gridDim.x * nwarps;
-    uint32_t *cb = GSTATE ? p.gstate + (size_t)slot * p.cand_words : smem + p.inc_words + (size_t)warp * p.cand_words;
-    V *wu = reinterpret_cast<V *>(cb) + (size_t)is * 2 * K;             // own ledger window: usage after
-    uint32_t *wt = cb + (size_t)P * 2 * K * VW + (size_t)is * 2 * K;      // own ledger window: times
-    uint32_t *A = cb + (size_t)P * 2 * K * (VW + 1);     // [P][m] F end, then B end   (time<<2 | state)
-    uint32_t *X = A + (size_t)P * m;                      // [P][m] offload end, then reload end
-    uint32_t *offm = X + (size_t)P * m;                   // [P][MW] offloaded bits
-    uint32_t *poff = offm + (size_t)P * MW;               // [P][MW] pending offload requests
-    uint32_t *prel = poff + (size_t)P * MW;               // [P][MW] pending reload requests
-    uint32_t *A_i = A + (size_t)is * m;
-    uint32_t *X_i = X + (size_t)is * m;
-    uint32_t *offm_i = offm + is * MW;
-    uint32_t *poff_i = poff + is * MW;
-    uint32_t *prel_i = prel + is * MW;
+    // State words are addressed as 32-bit offsets from the shared-memory symbol (or from the
+    // warp's global scratch slot): no 64-bit pointers stay live across the event loop.
+    uint32_t *const gsw = GSTATE ? p.gstate + (size_t)slot * p.cand_words : nullptr;
+    const int sbase = p.inc_words + warp * p.cand_words;       // shared-memory word offset
+#define SW(off) (GSTATE ? gsw[(off)] : smem[sbase + (off)])
+#define SV(off) (GSTATE ? reinterpret_cast<V *>(gsw)[(off)] : reinterpret_cast<V *>(smem)[sbase / VW + (off)])
+    const int o_wu = is * 2 * K;                                // own ledger window: usage after (V units)
+    const int o_wt = P * 2 * K * VW + is * 2 * K;               // own ledger window: times
+    const int o_A = P * 2 * K * (VW + 1);                       // [P][m] F end, then B end (time<<2 | state)
+    const int o_Ai = o_A + is * m;
+    const int o_Xi = o_A + P * m + is * m;                      // [P][m] offload end, then reload end
+    const int o_offm = o_A + 2 * P * m + is * MW;               // [P][MW] offloaded bits
+    const int o_poff = o_offm + P * MW;                         // [P][MW] pending offload requests
+    const int o_prel = o_poff + P * MW;                         // [P][MW] pending reload requests
     const int nz = 2 * P * m + 3 * P * MW;               // words zeroed per candidate
 
     const int chan_i = has_stage ? __ldg(&p.chan[i]) : -1;
@@ -211,8 +212,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     // holding the usage AFTER it; slots [ws, we) of a 2K array, compacted when the end is reached.
     // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
     auto win_fold = [&](int line) {
-        while (ws < we && (int)wt[ws] < line) {
-            V u = wu[ws];
+        while (ws < we && (int)SW(o_wt + (ws)) < line) {
+            V u = SV(o_wu + (ws));
             peak = u > peak ? u : peak;
             base = u;
             ++ws;
@@ -226,30 +227,30 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         top += d;
         rF = rG = V(-1);                               // the ledger changed: drop cached answers
         int k = we - 1;
-        while (k >= ws && (int)wt[k] > t) --k;         // last breakpoint at or before t
-        if (k >= ws && (int)wt[k] == t) {              // same time: merge into that breakpoint
-            for (int q = k; q < we; ++q) wu[q] += d;
+        while (k >= ws && (int)SW(o_wt + (k)) > t) --k;         // last breakpoint at or before t
+        if (k >= ws && (int)SW(o_wt + (k)) == t) {              // same time: merge into that breakpoint
+            for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;
             return;
         }
         if (we - ws == K) { ovf = true; return; }
         if (we == 2 * K) {                             // compact to the front
-            for (int q = ws; q < we; ++q) { wt[q - ws] = wt[q]; wu[q - ws] = wu[q]; }
+            for (int q = ws; q < we; ++q) { SW(o_wt + (q - ws)) = SW(o_wt + (q)); SV(o_wu + (q - ws)) = SV(o_wu + (q)); }
             k -= ws;
             we -= ws;
             ws = 0;
         }
-        for (int q = we - 1; q > k; --q) { wt[q + 1] = wt[q]; wu[q + 1] = wu[q] + d; }
-        wt[k + 1] = (uint32_t)t;
-        wu[k + 1] = (k >= ws ? wu[k] : base) + d;
+        for (int q = we - 1; q > k; --q) { SW(o_wt + (q + 1)) = SW(o_wt + (q)); SV(o_wu + (q + 1)) = SV(o_wu + (q)) + d; }
+        SW(o_wt + (k + 1)) = (uint32_t)t;
+        SV(o_wu + (k + 1)) = (k >= ws ? SV(o_wu + (k)) : base) + d;
         ++we;
     };
     // earliest_fit core: first breakpoint after the last one whose usage exceeds R.
     auto win_tau = [&](V R) -> int {
         if (R < 0 || top > R) return TAU_NONE;
         int k = we - 1;
-        while (k >= ws && !(wu[k] > R)) --k;
-        if (k >= ws) return (int)wt[k + 1];
-        return base > R && ws < we ? (int)wt[ws] : TAU_ANY;
+        while (k >= ws && !(SV(o_wu + (k)) > R)) --k;
+        if (k >= ws) return (int)SW(o_wt + (k + 1));
+        return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
     };
     auto tau_F = [&](V R) -> int {
         if (R != rF) { tauF = win_tau(R); rF = R; }
@@ -268,26 +269,26 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (k == KIND_F) {
             fl = 0;
             if (i > 0) {
-                uint32_t a = A[(i - 1) * m + j];
+                uint32_t a = SW(o_A + ((i - 1) * m + j));
                 if (!(a & 3u)) return;
                 fl = (int)(a >> 2) + p.comm;
             }
         } else if (k == KIND_B) {
-            uint32_t a = A_i[j];
+            uint32_t a = SW(o_Ai + (j));
             if ((a & 3u) != 1u) return;
             fl = (int)(a >> 2);
             if (i < P - 1) {
-                uint32_t b = A[(i + 1) * m + j];
+                uint32_t b = SW(o_A + ((i + 1) * m + j));
                 if ((b & 3u) != 2u) return;
                 fl = max(fl, (int)(b >> 2) + p.comm);
             }
-            if ((offm_i[j >> 5] >> (j & 31)) & 1u) {
-                uint32_t x = X_i[j];
+            if ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) {
+                uint32_t x = SW(o_Xi + (j));
                 if ((x & 3u) != 2u) return;
                 fl = max(fl, (int)(x >> 2));
             }
         } else {
-            uint32_t a = A_i[j];
+            uint32_t a = SW(o_Ai + (j));
             if ((a & 3u) != 2u) return;
             fl = (int)(a >> 2);
         }
@@ -304,37 +305,37 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto transfer_key = [&]() {
         uint32_t bh = KEY_NONE, bl = KEY_NONE;
         const int C = cfree;
-        const uint32_t sb = (uint32_t)i << 24;
+        const uint32_t stb = (uint32_t)i << 24;
         if (derived) {
             if (n_poff)
                 for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = poff_i[w]; bits; bits &= bits - 1) {
+                    for (uint32_t bits = SW(o_poff + (w)); bits; bits &= bits - 1) {
                         int j = w * 32 + __ffs(bits) - 1;
-                        uint32_t h = (uint32_t)max((int)(A_i[j] >> 2), C), l = (2u << 30) | sb | ((uint32_t)j << 2);
+                        uint32_t h = (uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C), l = (2u << 30) | stb | ((uint32_t)j << 2);
                         if (key_less(h, l, bh, bl)) { bh = h; bl = l; }
                     }
             if (n_prel)
                 for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = prel_i[w]; bits; bits &= bits - 1) {
+                    for (uint32_t bits = SW(o_prel + (w)); bits; bits &= bits - 1) {
                         int j = w * 32 + __ffs(bits) - 1;
                         int tau = tau_G(limit_i - val_of(j, 3));
                         if (tau == TAU_NONE) continue;
-                        uint32_t h = (uint32_t)max(max((int)(X_i[j] >> 2), C), tau);
-                        uint32_t l = (1u << 30) | sb | ((uint32_t)j << 2);
+                        uint32_t h = (uint32_t)max(max((int)(SW(o_Xi + (j)) >> 2), C), tau);
+                        uint32_t l = (1u << 30) | stb | ((uint32_t)j << 2);
                         if (key_less(h, l, bh, bl)) { bh = h; bl = l; }
                     }
         } else if (chead != NO_CHAN && (int)((chead >> 16) & 0x7FFFu) == i) {
             int j = chead & 0xFFFFu;
             if (!(chead >> 31)) {
-                uint32_t a = A_i[j];
-                if (a & 3u) { bh = (uint32_t)max((int)(a >> 2), C); bl = (2u << 30) | sb | ((uint32_t)j << 2); }
+                uint32_t a = SW(o_Ai + (j));
+                if (a & 3u) { bh = (uint32_t)max((int)(a >> 2), C); bl = (2u << 30) | stb | ((uint32_t)j << 2); }
             } else {
-                uint32_t x = X_i[j];
+                uint32_t x = SW(o_Xi + (j));
                 if ((x & 3u) == 1u) {
                     int tau = tau_G(limit_i - val_of(j, 3));
                     if (tau != TAU_NONE) {
                         bh = (uint32_t)max(max((int)(x >> 2), C), tau);
-                        bl = (1u << 30) | sb | ((uint32_t)j << 2);
+                        bl = (1u << 30) | stb | ((uint32_t)j << 2);
                     }
                 }
             }
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     for (long long item = slot; item < n_items; item += nslots) {
         cand = p.work_list ? (long long)p.work_list[item] : item;
         // ================= initialise ======================================================
-        for (int k = lane; k < nz; k += 32) A[k] = 0u;
+        for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = 0u;
         if (MOVES) {
             uint64_t gidx = (uint64_t)(p.first_index + cand);
             mv = decode_move(p.seed, p.round, gidx, P, m, p.shift_permille, p.max_shift, p.any_off != 0,
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 const int nb = m - w * 32;
                 if (nb < 32) bits &= (1u << nb) - 1u;
                 if (MOVES && mv.type == MOVE_TOGGLE && mv.stage == i && (mv.mb >> 5) == w) bits ^= 1u << (mv.mb & 31);
-                offm_i[w] = bits;
+                SW(o_offm + (w)) = bits;
                 n += __popc(bits);
                 // an offload bit on a non-offloadable op is malformed (KeyError in the reference)
                 if (check)
@@ -423,13 +424,13 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 for (int q = 0; q < L; ++q) {
                     uint32_t op = __ldg(&p.orders[((size_t)cand * P + i) * p.stride + q]);
                     uint32_t j = op >> 2, k = op & 3u;
-                    if (j >= (uint32_t)m || k > 2u || (A_i[j] >> k) & 1u) { bad = true; break; }
-                    A_i[j] |= 1u << k;
+                    if (j >= (uint32_t)m || k > 2u || (SW(o_Ai + (j)) >> k) & 1u) { bad = true; break; }
+                    SW(o_Ai + (j)) |= 1u << k;
                 }
                 if (!bad)
                     for (int j = 0; j < m; ++j)
-                        if (A_i[j] != 7u) { bad = true; break; }
-                for (int j = 0; j < m; ++j) A_i[j] = 0u;
+                        if (SW(o_Ai + (j)) != 7u) { bad = true; break; }
+                for (int j = 0; j < m; ++j) SW(o_Ai + (j)) = 0u;
             }
         }
         if (__any_sync(0xffffffffu, bad)) {
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                         const int gb = i * m + w * 32, qq = gb >> 5, sh = gb & 31;
                         uint32_t bb = (qq < mwords ? p.base_mask[qq] : 0u) >> sh;
                         if (sh && qq + 1 < mwords) bb |= p.base_mask[qq + 1] << (32 - sh);
-                        for (uint32_t x = (offm_i[w] ^ bb) & (m - w * 32 < 32 ? (1u << (m - w * 32)) - 1u : ~0u); x; x &= x - 1)
+                        for (uint32_t x = (SW(o_offm + (w)) ^ bb) & (m - w * 32 < 32 ? (1u << (m - w * 32)) - 1u : ~0u); x; x &= x - 1)
                             d = min(d, p.fstep[i * m + w * 32 + __ffs(x) - 1]);
                     }
                 }
@@ -498,18 +499,18 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 __syncwarp();
                 continue;
             }
-            for (int k = lane; k < nz; k += 32) A[k] = src[k];
+            for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = src[k];
             if (has_stage) {
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
-                for (int q = 0; q < we; ++q) { wt[q] = st[q]; wu[q] = su[q]; }
+                for (int q = 0; q < we; ++q) { SW(o_wt + (q)) = st[q]; SV(o_wu + (q)) = su[q]; }
             }
             __syncwarp();
             if (has_stage) {
                 // this candidate's offload bits: any difference lies on an F the base has not
                 // committed yet, so only the outstanding-transfer count moves
                 int nb = 0;
-                for (int w = 0; w < MW; ++w) nb += __popc(offm_i[w]);
+                for (int w = 0; w < MW; ++w) nb += __popc(SW(o_offm + (w)));
                 n_unrel += cand_unrel - nb;
                 build_mask(false);
             }
@@ -540,11 +541,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 const int c = ecount / p.ck_interval;
                 if (c < p.ck_max) {
                     uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                    for (int q = lane; q < nz; q += 32) dst[q] = A[q];
+                    for (int q = lane; q < nz; q += 32) dst[q] = SW(o_A + (q));
                     if (has_stage) {
                         uint32_t *st = dst + ck_t + i * p.ck_kc;
                         V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
-                        for (int q = ws; q < we; ++q) { st[q - ws] = wt[q]; su[q - ws] = wu[q]; }
+                        for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
                     }
                     const int ws0 = ws, we0 = we;
                     we -= ws;
@@ -581,7 +582,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             if (rank == RANK_COMPUTE) {
                 if (i == w) {
                     const int end = t + proc_of(j, k);
-                    const bool newreq = derived && k == KIND_F && ((offm_i[j >> 5] >> (j & 31)) & 1u);
+                    const bool newreq = derived && k == KIND_F && ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u);
                     win_insert(end, val_of(j, k));
                     sfree = end;
                     ++pos;
@@ -589,11 +590,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     nxt = fetch(pos + 1);
                     if (first_start == INT_MAX) first_start = t;
                     if (k == KIND_F) {
-                        A_i[j] = ((uint32_t)end << 2) | 1u;
+                        SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
                         if (first_f == INT_MAX) first_f = t;
-                        if (newreq) { poff_i[j >> 5] |= 1u << (j & 31); ++n_poff; }
+                        if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
                     } else if (k == KIND_B) {
-                        A_i[j] = ((uint32_t)end << 2) | 2u;
+                        SW(o_Ai + (j)) = ((uint32_t)end << 2) | 2u;
                     } else {
                         last_w = end;
                     }
@@ -613,14 +614,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     const V g = val_of(j, 3);
                     const uint32_t bit = 1u << (j & 31);
                     if (rank == RANK_OFFLOAD) {
-                        X_i[j] = ((uint32_t)end << 2) | 1u;
+                        SW(o_Xi + (j)) = ((uint32_t)end << 2) | 1u;
                         win_insert(end, -g);
-                        if (derived) { poff_i[j >> 5] &= ~bit; prel_i[j >> 5] |= bit; --n_poff; ++n_prel; }
+                        if (derived) { SW(o_poff + (j >> 5)) &= ~bit; SW(o_prel + (j >> 5)) |= bit; --n_poff; ++n_prel; }
                     } else {
-                        X_i[j] = ((uint32_t)end << 2) | 2u;
+                        SW(o_Xi + (j)) = ((uint32_t)end << 2) | 2u;
                         win_insert(t, g);
                         --n_unrel;
-                        if (derived) { prel_i[j >> 5] &= ~bit; --n_prel; }
+                        if (derived) { SW(o_prel + (j >> 5)) &= ~bit; --n_prel; }
                     }
                     // the ledger changed: an F head re-fits; a B head may have been waiting on this reload
                     cdirty = cdirty || (pos < L && ((head & 3u) == KIND_F || head == (((uint32_t)j << 2) | KIND_B)));
@@ -693,6 +694,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
         __syncwarp();
     }
+#undef SW
+#undef SV
 }
 
 }  // namespace ps
