@@ -46,11 +46,12 @@ def _events_from_trace(pk, codes, starts, count, types):
     """Rebuild commit-ordered events from the kernel trace (include/pipesched_b200.h)."""
     compute, transfers = [], []
     Reload, Offload = types.TransferKind.RELOAD, types.TransferKind.OFFLOAD
+    Op, Kind = getattr(types, "OpId", OpId), getattr(types, "OpKind", OpKind)   # the caller's op types
     for q in range(count):
         code = int(codes[q]) & 0xFFFFFFFF
         t = int(starts[q])
         rank, i0, j0, k = code >> 30, (code >> 24) & 63, (code >> 2) & 0x3FFFFF, code & 3
-        op = OpId(i0 + 1, j0 + 1, OpKind(k))
+        op = Op(i0 + 1, j0 + 1, Kind(k))
         if rank == 0:
             compute.append(types.ComputeEvent(op, t, t + int(pk.proc_time[i0, j0, k])))
         else:
