@@ -1,0 +1,112 @@
+"""Batched re-timing of cached schedule orders.
+
+The reference cache stores solved *orders* (per-stage op orders, offloaded set,
+per-channel transfer orders) and re-times them for a new instance with
+``run_order`` in explicit channel-order mode, rejecting entries that deadlock
+or fail STRICT validation (cache.py:224-240); ``warm_start_from_cache``
+compares the adapted hit with the heuristics, the cache winning ties
+(cache.py:243-259).  Here every candidate entry is re-timed in ONE kernel
+launch (``run_orders(..., explicit=True)``).  Entries are read in the
+reference's JSON-lines record format (CacheEntry.to_dict, cache.py:78-92);
+the file store, locking and fingerprint lookup stay in the reference.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+from .instance import OpId, OpKind
+from .schedule import MemorySemantics, TransferKind, makespan, validate
+
+
+class ShapeMismatch(Exception):
+    """Entry and instance disagree on (stages, micro-batches)."""
+
+
+@dataclass(frozen=True)
+class CachedOrder:
+    num_stages: int
+    num_microbatches: int
+    stage_orders: tuple       # per stage (1-based position) tuple of OpId
+    offloaded: frozenset
+    channel_orders: tuple     # per channel tuple of (OpId, TransferKind)
+    recorded_makespan_ratio: float = 0.0
+
+
+def entry_from_record(d: dict) -> CachedOrder:
+    """One JSON-lines record of the reference cache (cache.py:78-106)."""
+    order = d["order"]
+    stages = tuple(tuple(OpId(i + 1, int(j), OpKind.from_letter(c)) for j, c in so)
+                   for i, so in enumerate(order["stages"]))
+    off = frozenset(OpId(int(i), int(j), OpKind.F) for i, j in order["offloaded"])
+    chans = tuple(tuple((OpId(int(i), int(j), OpKind.from_letter(c)),
+                         TransferKind.OFFLOAD if t == "O" else TransferKind.RELOAD)
+                        for i, j, c, t in co) for co in order["channels"])
+    return CachedOrder(int(d["key"]["P"]), int(d["key"]["m"]), stages, off, chans,
+                       float(d.get("makespan_ratio", 0.0)))
+
+
+def load_entries(path) -> list:
+    out = []
+    with open(path, encoding="utf-8") as fh:
+        for line in fh:
+            if line.strip():
+                out.append(entry_from_record(json.loads(line)))
+    return out
+
+
+def _shape(entry):
+    key = getattr(entry, "key", None)
+    if key is not None:
+        return key.num_stages, key.num_microbatches
+    return entry.num_stages, entry.num_microbatches
+
+
+def adapt_batch(entries, inst, device=None) -> list:
+    """Re-time every entry for `inst` in one launch: a Schedule, or None when the order deadlocks
+    or the result fails STRICT validation (cache.py:224-240)."""
+    from .listsched import OrderInfeasible, run_orders
+    for e in entries:
+        if _shape(e) != (inst.num_stages, inst.num_microbatches):
+            raise ShapeMismatch(f"entry is {_shape(e)[0]}x{_shape(e)[1]}, instance is "
+                                f"{inst.num_stages}x{inst.num_microbatches}")
+    cands = []
+    for e in entries:
+        orders = {i + 1: tuple(e.stage_orders[i]) for i in range(len(e.stage_orders))}
+        chans = {g: tuple(e.channel_orders[g]) for g in range(len(e.channel_orders))}
+        cands.append((orders, frozenset(e.offloaded), chans))
+    res = run_orders(inst, cands, explicit=True, device=device) if cands else []
+    out = []
+    for r in res:
+        if isinstance(r, OrderInfeasible) or not validate(r, inst, MemorySemantics.STRICT).ok:
+            out.append(None)
+        else:
+            out.append(r)
+    return out
+
+
+def adapt(entry, inst, device=None):
+    return adapt_batch([entry], inst, device)[0]
+
+
+def best_adapted(entries, inst, device=None):
+    """(schedule, index) of the minimum-makespan adaptable entry, first wins ties; or (None, None)."""
+    best = (None, None, None)
+    for k, s in enumerate(adapt_batch(entries, inst, device)):
+        if s is None:
+            continue
+        span = makespan(s, inst)
+        if best[0] is None or span < best[0]:
+            best = (span, s, k)
+    return best[1], best[2]
+
+
+def warm_start_from_entries(entries, inst, params=None, device=None):
+    """Best of the adapted entries and the heuristics; the cache wins ties (cache.py:243-259)."""
+    from .heuristics import AdaParams, best_feasible
+    adapted, _ = best_adapted(entries, inst, device)
+    fallback, name = best_feasible(inst, params or AdaParams(), device=device)
+    if adapted is not None and makespan(adapted, inst) <= makespan(fallback, inst):
+        return adapted, "cache"
+    return fallback, name

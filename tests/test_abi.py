@@ -61,3 +61,15 @@ def test_product_path_fails_loudly_without_cuda(monkeypatch):
     inst = make_uniform_instance(1, 1, 1, 1, 1, 0, 1, 2, 4)
     with pytest.raises(_native.NativeUnavailable):
         run_order(inst, {1: tuple(inst.stage_ops(1))}, frozenset())
+
+
+def test_cache_records_parse_in_the_reference_format(tmp_path):
+    from paper_2510_05186_b200.cache import load_entries
+    rec = ('{"key": {"P": 1, "m": 1, "ratios": [1.0, 1.0, 0.0, 1.0, 2.0], "post_validation": false}, '
+           '"order": {"stages": [[[1, "F"], [1, "B"], [1, "W"]]], "offloaded": [[1, 1]], '
+           '"channels": [[[1, 1, "F", "O"], [1, 1, "F", "R"]]]}, "makespan_ratio": 3.0}')
+    p = tmp_path / "cache.jsonl"
+    p.write_text(rec + "\n")
+    (e,) = load_entries(p)
+    assert e.num_stages == 1 and len(e.stage_orders[0]) == 3 and len(e.channel_orders[0]) == 2
+    assert e.channel_orders[0][1][1].value == "reload"
