@@ -165,3 +165,21 @@ def test_prefix_sharing_is_exact(cuda_ok, cfg):
     o2[0, 0, :2] = torch.flip(row[:2], [0])
     bad.record(o2[0], mk[1])
     _eval_both(ls.di, o, mk, bad)
+
+
+def test_host_buffer_path_matches_device_path(cuda_ok):
+    """ps_eval_batch_host (chunked, copies overlapped) == ps_eval_batch on the same candidates."""
+    import torch
+    inst, orders, off, LocalSearch, SearchConfig = _setup(3)
+    n = 20000                      # several pipeline chunks
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n))
+    o, mk = ls.materialize(0, n, 0)
+    dev = ls.di.evaluate(o, mk, peak=True)
+    torch.cuda.synchronize()
+    h_o = o.cpu().numpy()
+    h_m = mk.cpu().numpy()
+    for base in (None, ls.base):
+        host = ls.di.evaluate_host(h_o, h_m, peak=True, base=base)
+        assert (host.flags == dev.flags.cpu().numpy()).all()
+        assert (host.makespan == dev.makespan.cpu().numpy()).all()
+        assert (host.peak == dev.peak.cpu().numpy()).all()
