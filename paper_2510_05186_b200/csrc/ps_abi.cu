@@ -117,13 +117,20 @@ int incumbent_words(const ps_instance *I, bool moves) {
     return (w + 3) & ~3;
 }
 
-cudaError_t occupancy(bool v64, bool moves, bool gstate, int block, size_t smem, int *n) {
-    return v64 ? eval_occupancy<long long>(moves, gstate, block, smem, n) : eval_occupancy<int>(moves, gstate, block, smem, n);
+cudaError_t occupancy(bool v64, bool moves, Variant v, int block, size_t smem, int *n) {
+    if (v64) return moves ? eval_occupancy<long long, true>(v, block, smem, n) : eval_occupancy<long long, false>(v, block, smem, n);
+    return moves ? eval_occupancy<int, true>(v, block, smem, n) : eval_occupancy<int, false>(v, block, smem, n);
 }
 
 cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s,
                    bool record = false) {
-    return v64 ? eval_launch<long long>(moves, gstate, record, p, c, s) : eval_launch<int>(moves, gstate, record, p, c, s);
+    Variant v;
+    v.gstate = gstate;
+    v.record = record;
+    v.derived = p.chorders == nullptr;
+    v.uni = p.uniform != 0;
+    if (v64) return moves ? eval_launch<long long, true>(v, p, c, s) : eval_launch<long long, false>(v, p, c, s);
+    return moves ? eval_launch<int, true>(v, p, c, s) : eval_launch<int, false>(v, p, c, s);
 }
 
 int env_int(const char *name, int dflt) {
@@ -165,7 +172,12 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl) {
         return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
     pl->cfg.block = 32 * pl->warps;
     int per_sm = 0;
-    cudaError_t e = occupancy(I->v64, moves, pl->gstate, pl->cfg.block, pl->cfg.smem, &per_sm);
+    Variant v;
+    v.gstate = pl->gstate;
+    v.record = false;
+    v.derived = true;
+    v.uni = I->uniform != 0;
+    cudaError_t e = occupancy(I->v64, moves, v, pl->cfg.block, pl->cfg.smem, &per_sm);
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     if (per_sm < 1) per_sm = 1;
     int64_t want = (N + pl->warps - 1) / pl->warps;

@@ -109,7 +109,8 @@ __device__ __forceinline__ bool key_less(uint32_t ah, uint32_t al, uint32_t bh, 
 #define PS_MIN_BLOCKS 8
 #endif
 
-template <typename V, bool MOVES, bool GSTATE, bool REC>
+// DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
+template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
 __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval_kernel(const EvalParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     const int i = lane;                               // the stage this lane owns
     const bool has_stage = i < P;
     const int is = has_stage ? i : 0;
-    const bool derived = p.chorders == nullptr;
+    constexpr bool derived = DERIVED;
 
     // ---- block-shared incumbent (move mode) ---------------------------------------------
     uint16_t *inc_s = reinterpret_cast<uint16_t *>(smem);
@@ -154,11 +155,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
 
     const int chan_i = has_stage ? __ldg(&p.chan[i]) : -1;
     const V limit_i = has_stage ? ldv<V>(p.limit, i) : V(0);
-    const int rowbase = p.uniform ? is : is * m;
+    const int rowbase = UNI ? is : is * m;
     // per-stage constants of microbatch-symmetric instances live in registers
     int t0 = 0, t1 = 0, t2 = 0;
     V v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-    if (p.uniform) {
+    if (UNI) {
         t0 = __ldg(&p.proc[rowbase * 3 + 0]);
         t1 = __ldg(&p.proc[rowbase * 3 + 1]);
         t2 = __ldg(&p.proc[rowbase * 3 + 2]);
@@ -168,11 +169,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         v3 = ldv<V>(p.vals, rowbase * 4 + 3);
     }
     auto proc_of = [&](int j, int k) -> int {
-        if (p.uniform) return k == 0 ? t0 : (k == 1 ? t1 : t2);
+        if (UNI) return k == 0 ? t0 : (k == 1 ? t1 : t2);
         return __ldg(&p.proc[(rowbase + j) * 3 + k]);
     };
     auto val_of = [&](int j, int k) -> V {
-        if (p.uniform) return k == 0 ? v0 : (k == 1 ? v1 : (k == 2 ? v2 : v3));
+        if (UNI) return k == 0 ? v0 : (k == 1 ? v1 : (k == 2 ? v2 : v3));
         return ldv<V>(p.vals, (rowbase + j) * 4 + k);
     };
 
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     int n_poff = 0, n_prel = 0, n_unrel = 0;   // pending offloads / reloads / offloaded not yet reloaded
     V rF = V(-1), rG = V(-1);                  // earliest_fit cache, valid until the ledger changes
     int tauF = 0, tauG = 0;
-    int first_start = INT_MAX, first_f = INT_MAX, last_w = 0;
+    int first_start = INT_MAX;      // start of the stage's first op (always an F; its last op is always a W)
     int ecount = 0, ecount0 = 0;             // events committed / restored from a checkpoint
     uint32_t head = 0, nxt = 0;
     int cpos = 0;
@@ -365,14 +366,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     const int ck_r = ck_u + P * p.ck_kc * VW;
     auto save_regs = [&](uint32_t *rg) {
         rg[0] = pos; rg[1] = sfree; rg[2] = cfree; rg[3] = ws; rg[4] = we; rg[5] = n_poff; rg[6] = n_prel;
-        rg[7] = n_unrel; rg[8] = first_start; rg[9] = first_f; rg[10] = last_w;
+        rg[7] = n_unrel; rg[8] = first_start;
         *reinterpret_cast<long long *>(rg + 12) = (long long)base;
         *reinterpret_cast<long long *>(rg + 14) = (long long)top;
         *reinterpret_cast<long long *>(rg + 16) = (long long)peak;
     };
     auto load_regs = [&](const uint32_t *rg) {
         pos = rg[0]; sfree = rg[1]; cfree = rg[2]; ws = rg[3]; we = rg[4]; n_poff = rg[5]; n_prel = rg[6];
-        n_unrel = rg[7]; first_start = rg[8]; first_f = rg[9]; last_w = rg[10];
+        n_unrel = rg[7]; first_start = rg[8];
         base = (V)*reinterpret_cast<const long long *>(rg + 12);
         top = (V)*reinterpret_cast<const long long *>(rg + 14);
         peak = (V)*reinterpret_cast<const long long *>(rg + 16);
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (MOVES) {
             uint64_t gidx = (uint64_t)(p.first_index + cand);
             mv = decode_move(p.seed, p.round, gidx, P, m, p.shift_permille, p.max_shift, p.any_off != 0,
-                             [&](int s, int j) { return ldv<V>(p.vals, (p.uniform ? s : s * m + j) * 4 + 3) > V(0); });
+                             [&](int s, int j) { return ldv<V>(p.vals, (UNI ? s : s * m + j) * 4 + 3) > V(0); });
         }
         __syncwarp();
         bool bad = false;
@@ -522,7 +523,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             base = top = peak = 0; ws = we = 0;
             n_poff = n_prel = 0;
             n_unrel = cand_unrel;
-            first_start = INT_MAX; first_f = INT_MAX; last_w = 0; ecount = 0;
+            first_start = INT_MAX; ecount = 0;
         }
         ovf = false;
         rF = rG = V(-1);
@@ -591,12 +592,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     if (first_start == INT_MAX) first_start = t;
                     if (k == KIND_F) {
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
-                        if (first_f == INT_MAX) first_f = t;
                         if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
                     } else if (k == KIND_B) {
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 2u;
-                    } else {
-                        last_w = end;
                     }
                     cdirty = true;
                     // reload keys read the ledger; a new request or explicit channel head may appear
@@ -646,7 +644,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             long long span = -1;
             if (!unusable && rem == 0u) {
                 win_fold(INT_MAX);
-                int hi = p.post ? (has_stage ? last_w - first_f : 0) : (has_stage ? sfree : 0);
+                int hi = p.post ? (has_stage ? sfree - first_start : 0) : (has_stage ? sfree : 0);
                 int lo = p.post ? 0 : (has_stage ? first_start : INT_MAX);
                 span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, lo);
             }
@@ -671,7 +669,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             win_fold(INT_MAX);
             int hi, lo;
             if (p.post) {
-                hi = has_stage ? last_w - first_f : 0;
+                hi = has_stage ? sfree - first_start : 0;
                 lo = 0;
             } else {
                 hi = has_stage ? sfree : 0;

@@ -1,37 +1,54 @@
-// ps_eval_impl.cuh — instantiation helpers for ps_launch.h (included once per ledger width).
+// ps_eval_impl.cuh — instantiation helpers for ps_launch.h (included once per (V, MOVES) TU).
 #pragma once
 #include "ps_launch.h"
 
 namespace ps {
 
-template <typename V, bool MOVES, bool GSTATE, bool REC>
+template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
 static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t stream) {
-    auto fn = eval_kernel<V, MOVES, GSTATE, REC>;
+    auto fn = eval_kernel<V, MOVES, GSTATE, REC, DERIVED, UNI>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
     if (e != cudaSuccess) return e;
     fn<<<cfg.grid, cfg.block, cfg.smem, stream>>>(p);
     return cudaGetLastError();
 }
 
-template <typename V, bool MOVES, bool GSTATE>
+template <typename V, bool MOVES, bool GSTATE, bool DERIVED, bool UNI>
 static cudaError_t occ_one(int block, size_t smem, int *n) {
-    auto fn = eval_kernel<V, MOVES, GSTATE, false>;
+    auto fn = eval_kernel<V, MOVES, GSTATE, false, DERIVED, UNI>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, fn, block, smem);
 }
 
-template <typename V>
-cudaError_t eval_launch(bool moves, bool gstate, bool record, const EvalParams &p, LaunchCfg cfg, cudaStream_t s) {
-    if (record) return launch_one<V, false, false, true>(p, cfg, s);
-    if (moves) return gstate ? launch_one<V, true, true, false>(p, cfg, s) : launch_one<V, true, false, false>(p, cfg, s);
-    return gstate ? launch_one<V, false, true, false>(p, cfg, s) : launch_one<V, false, false, false>(p, cfg, s);
+// Move-encoded candidates (the search) are always in derived channel mode; base recording is a
+// single materialised candidate in derived mode with its state in shared memory.
+#define PS_PICK(FN, ARGS)                                                                              \
+    if (!MOVES && v.record)                                                                           \
+        return v.uni ? FN<V, false, false, true, true, true> ARGS : FN<V, false, false, true, true, false> ARGS; \
+    if (MOVES || v.derived) {                                                                         \
+        if (v.gstate) return v.uni ? FN<V, MOVES, true, false, true, true> ARGS : FN<V, MOVES, true, false, true, false> ARGS; \
+        return v.uni ? FN<V, MOVES, false, false, true, true> ARGS : FN<V, MOVES, false, false, true, false> ARGS; \
+    }                                                                                                 \
+    if (v.gstate) return v.uni ? FN<V, false, true, false, false, true> ARGS : FN<V, false, true, false, false, false> ARGS; \
+    return v.uni ? FN<V, false, false, false, false, true> ARGS : FN<V, false, false, false, false, false> ARGS;
+
+#define PS_PICK_OCC(FN, ARGS)                                                                          \
+    if (MOVES || v.derived) {                                                                         \
+        if (v.gstate) return v.uni ? FN<V, MOVES, true, true, true> ARGS : FN<V, MOVES, true, true, false> ARGS; \
+        return v.uni ? FN<V, MOVES, false, true, true> ARGS : FN<V, MOVES, false, true, false> ARGS; \
+    }                                                                                                 \
+    if (v.gstate) return v.uni ? FN<V, false, true, false, true> ARGS : FN<V, false, true, false, false> ARGS; \
+    return v.uni ? FN<V, false, false, false, true> ARGS : FN<V, false, false, false, false> ARGS;
+
+template <typename V, bool MOVES>
+cudaError_t eval_launch(Variant v, const EvalParams &p, LaunchCfg cfg, cudaStream_t s) {
+    PS_PICK(launch_one, (p, cfg, s))
 }
 
-template <typename V>
-cudaError_t eval_occupancy(bool moves, bool gstate, int block, size_t smem, int *n) {
-    if (moves) return gstate ? occ_one<V, true, true>(block, smem, n) : occ_one<V, true, false>(block, smem, n);
-    return gstate ? occ_one<V, false, true>(block, smem, n) : occ_one<V, false, false>(block, smem, n);
+template <typename V, bool MOVES>
+cudaError_t eval_occupancy(Variant v, int block, size_t smem, int *n) {
+    PS_PICK_OCC(occ_one, (block, smem, n))
 }
 
 }  // namespace ps

@@ -1,4 +1,4 @@
-// ps_launch.h — host-side launch interface of the evaluator variants (one TU per ledger width).
+// ps_launch.h — host-side launch interface of the evaluator variants.
 #pragma once
 #include <cuda_runtime.h>
 #include "ps_eval.cuh"
@@ -10,11 +10,17 @@ struct LaunchCfg {
     size_t smem;
 };
 
-// Variant = (ledger value type V, move-encoded candidates, state in global memory, base recording).
-template <typename V>
-cudaError_t eval_launch(bool moves, bool gstate, bool record, const EvalParams &p, LaunchCfg cfg,
-                        cudaStream_t stream);
-template <typename V>
-cudaError_t eval_occupancy(bool moves, bool gstate, int block, size_t smem, int *blocks_per_sm);
+struct Variant {
+    bool gstate;    // per-candidate state in global memory
+    bool record;    // base recording (checkpoints)
+    bool derived;   // greedy channel mode
+    bool uni;       // microbatch-symmetric instance tables
+};
+
+// One translation unit per (ledger value type V, move-encoded candidates).
+template <typename V, bool MOVES>
+cudaError_t eval_launch(Variant v, const EvalParams &p, LaunchCfg cfg, cudaStream_t stream);
+template <typename V, bool MOVES>
+cudaError_t eval_occupancy(Variant v, int block, size_t smem, int *blocks_per_sm);
 
 }  // namespace ps
