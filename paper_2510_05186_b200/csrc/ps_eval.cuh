@@ -99,14 +99,19 @@ __device__ __forceinline__ V ldv(const void *base, int idx) {
     return __ldg(reinterpret_cast<const V *>(base) + idx);
 }
 
-__device__ __forceinline__ bool key_less(uint32_t ah, uint32_t al, uint32_t bh, uint32_t bl) {
-    return ah < bh || (ah == bh && al < bl);
+// A candidate key: start in the high word, (rank, stage, microbatch, kind) in the low word.
+__device__ __forceinline__ unsigned long long make_key(uint32_t hi, uint32_t lo) {
+    return ((unsigned long long)hi << 32) | lo;
 }
+constexpr unsigned long long KEY_ABSENT = ~0ull;
 
 // 64 registers per thread (8 blocks of 4 warps per SM) measured best on B200 for the
 // shared-memory variants (tools/kexp.py); the global-state variant keeps its registers.
 #ifndef PS_MIN_BLOCKS
 #define PS_MIN_BLOCKS 8
+#endif
+#ifndef PS_TAU_PAIR
+#define PS_TAU_PAIR 0   // measured slower on B200 (r01): register pressure outweighs the saved scan
 #endif
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
@@ -182,13 +187,15 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     Move mv;
     mv.type = MOVE_NOOP; mv.stage = 0; mv.a = mv.b = 0; mv.mb = 0;
     int pos = 0, sfree = 0, cfree = 0;
-    uint32_t ckh = KEY_NONE, ckl = KEY_NONE;   // cached compute-head key
-    uint32_t tkh = KEY_NONE, tkl = KEY_NONE;   // cached best transfer key of this stage
+    unsigned long long ckey = KEY_ABSENT;      // cached compute-head key
+    unsigned long long tkey = KEY_ABSENT;      // cached best transfer key of this stage
     bool cdirty = false, tdirty = false, ovf = false;
     V base = 0, top = 0, peak = 0;
     int ws = 0, we = 0;
     int n_poff = 0, n_prel = 0, n_unrel = 0;   // pending offloads / reloads / offloaded not yet reloaded
-    V rF = V(-1), rG = V(-1);                  // earliest_fit cache, valid until the ledger changes
+    // earliest_fit cache, valid until the ledger changes; NO_R marks it empty (R >= -delta > NO_R)
+    constexpr V NO_R = (V)(sizeof(V) == 8 ? (V)0x8000000000000000LL : (V)0x80000000);
+    V rF = NO_R, rG = NO_R;
     int tauF = 0, tauG = 0;
     int first_start = INT_MAX;      // start of the stage's first op (always an F; its last op is always a W)
     int ecount = 0, ecount0 = 0;             // events committed / restored from a checkpoint
@@ -226,7 +233,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto win_insert = [&](int t, V d) {
         win_fold(n_unrel > 0 ? min(sfree, cfree) : sfree);
         top += d;
-        rF = rG = V(-1);                               // the ledger changed: drop cached answers
+        rF = rG = NO_R;                                // the ledger changed: drop cached answers
         int k = we - 1;
         while (k >= ws && (int)SW(o_wt + (k)) > t) --k;         // last breakpoint at or before t
         if (k >= ws && (int)SW(o_wt + (k)) == t) {              // same time: merge into that breakpoint
@@ -253,17 +260,41 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (k >= ws) return (int)SW(o_wt + (k + 1));
         return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
     };
+    // Symmetric tables: the F and reload thresholds are per-stage constants with R_G >= R_F, so one
+    // backward scan finds the last breakpoint above R_F and, continuing, the last above R_G.
+    auto tau_pair = [&]() {
+        const V RF = limit_i - v0, RG = limit_i - v3;
+        int k = we - 1;
+        while (k >= ws && !(SV(o_wu + (k)) > RF)) --k;
+        const int kF = k;
+        while (k >= ws && !(SV(o_wu + (k)) > RG)) --k;
+        auto conv = [&](V R, int kk) -> int {
+            if (R < 0 || top > R) return TAU_NONE;
+            if (kk >= ws) return (int)SW(o_wt + (kk + 1));
+            return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
+        };
+        tauF = conv(RF, kF);
+        tauG = conv(RG, k);
+        rF = RF;
+        rG = RG;
+    };
     auto tau_F = [&](V R) -> int {
-        if (R != rF) { tauF = win_tau(R); rF = R; }
+        if (R != rF) {
+            if (UNI && PS_TAU_PAIR) tau_pair();
+            else { tauF = win_tau(R); rF = R; }
+        }
         return tauF;
     };
     auto tau_G = [&](V R) -> int {
-        if (R != rG) { tauG = win_tau(R); rG = R; }
+        if (R != rG) {
+            if (UNI && PS_TAU_PAIR) tau_pair();
+            else { tauG = win_tau(R); rG = R; }
+        }
         return tauG;
     };
 
     auto compute_key = [&]() {
-        ckh = ckl = KEY_NONE;
+        ckey = KEY_ABSENT;
         if (pos >= L) return;
         const int j = head >> 2, k = head & 3u;
         int fl;
@@ -299,12 +330,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             if (tau == TAU_NONE) return;
             if (tau != TAU_ANY) lo = max(lo, tau - proc_of(j, 0));
         }
-        ckh = (uint32_t)lo;
-        ckl = ((uint32_t)i << 24) | ((uint32_t)j << 2) | (uint32_t)k;
+        ckey = make_key((uint32_t)lo, ((uint32_t)i << 24) | ((uint32_t)j << 2) | (uint32_t)k);
     };
 
     auto transfer_key = [&]() {
-        uint32_t bh = KEY_NONE, bl = KEY_NONE;
+        unsigned long long best = KEY_ABSENT;
         const int C = cfree;
         const uint32_t stb = (uint32_t)i << 24;
         if (derived) {
@@ -312,8 +342,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 for (int w = 0; w < MW; ++w)
                     for (uint32_t bits = SW(o_poff + (w)); bits; bits &= bits - 1) {
                         int j = w * 32 + __ffs(bits) - 1;
-                        uint32_t h = (uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C), l = (2u << 30) | stb | ((uint32_t)j << 2);
-                        if (key_less(h, l, bh, bl)) { bh = h; bl = l; }
+                        best = min(best, make_key((uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C),
+                                                  (2u << 30) | stb | ((uint32_t)j << 2)));
                     }
             if (n_prel)
                 for (int w = 0; w < MW; ++w)
@@ -321,28 +351,25 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                         int j = w * 32 + __ffs(bits) - 1;
                         int tau = tau_G(limit_i - val_of(j, 3));
                         if (tau == TAU_NONE) continue;
-                        uint32_t h = (uint32_t)max(max((int)(SW(o_Xi + (j)) >> 2), C), tau);
-                        uint32_t l = (1u << 30) | stb | ((uint32_t)j << 2);
-                        if (key_less(h, l, bh, bl)) { bh = h; bl = l; }
+                        best = min(best, make_key((uint32_t)max(max((int)(SW(o_Xi + (j)) >> 2), C), tau),
+                                                  (1u << 30) | stb | ((uint32_t)j << 2)));
                     }
         } else if (chead != NO_CHAN && (int)((chead >> 16) & 0x7FFFu) == i) {
             int j = chead & 0xFFFFu;
             if (!(chead >> 31)) {
                 uint32_t a = SW(o_Ai + (j));
-                if (a & 3u) { bh = (uint32_t)max((int)(a >> 2), C); bl = (2u << 30) | stb | ((uint32_t)j << 2); }
+                if (a & 3u) best = make_key((uint32_t)max((int)(a >> 2), C), (2u << 30) | stb | ((uint32_t)j << 2));
             } else {
                 uint32_t x = SW(o_Xi + (j));
                 if ((x & 3u) == 1u) {
                     int tau = tau_G(limit_i - val_of(j, 3));
                     if (tau != TAU_NONE) {
-                        bh = (uint32_t)max(max((int)(x >> 2), C), tau);
-                        bl = (1u << 30) | stb | ((uint32_t)j << 2);
+                        best = make_key((uint32_t)max(max((int)(x >> 2), C), tau), (1u << 30) | stb | ((uint32_t)j << 2));
                     }
                 }
             }
         }
-        tkh = bh;
-        tkl = bl;
+        tkey = best;
     };
 
     // Lane 0 publishes a candidate's outcome (search rounds may pass no arrays).
@@ -526,11 +553,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             first_start = INT_MAX; ecount = 0;
         }
         ovf = false;
-        rF = rG = V(-1);
+        rF = rG = NO_R;
         head = fetch(pos); nxt = fetch(pos + 1);
         cpos = 0; chead = fetch_chan(0); cnext = fetch_chan(1);
         cdirty = tdirty = has_stage;
-        ckh = ckl = tkh = tkl = KEY_NONE;
+        ckey = tkey = KEY_ABSENT;
         __syncwarp();
 
         // ================= simulate: one committed event per iteration ===================
@@ -560,10 +587,10 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             }
             if (cdirty) { compute_key(); cdirty = false; }
             if (tdirty) { transfer_key(); tdirty = false; }
-            uint32_t kh = ckh, kl = ckl;
-            if (key_less(tkh, tkl, kh, kl)) { kh = tkh; kl = tkl; }
+            const unsigned long long key = min(ckey, tkey);
+            const uint32_t kh = (uint32_t)(key >> 32);
             const uint32_t mh = __reduce_min_sync(0xffffffffu, kh);
-            const uint32_t ml = __reduce_min_sync(0xffffffffu, kh == mh ? kl : 0xFFFFFFFFu);
+            const uint32_t ml = __reduce_min_sync(0xffffffffu, kh == mh ? (uint32_t)key : 0xFFFFFFFFu);
             if (mh == KEY_NONE) break;
 
             const int t = (int)mh;
