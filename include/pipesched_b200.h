@@ -140,7 +140,8 @@ int ps_instance_destroy(ps_instance *inst);
 int ps_instance_get_info(const ps_instance *inst, ps_instance_info *out);
 
 /* Base recording for prefix sharing.  ps_base_record copies the candidate (device buffers
-   [P][order_stride] and [mask_words]) and simulates it once, checkpointing as it goes. */
+   [P][order_stride] and [mask_words]) and simulates it once, checkpointing as it goes; it returns
+   after the recording (evaluations size their ledger window from what the base needed). */
 int ps_base_create(const ps_instance *inst, ps_base **out);
 int ps_base_destroy(ps_base *base);
 int ps_base_record(ps_base *base, const uint16_t *orders, const uint32_t *mask, void *stream);

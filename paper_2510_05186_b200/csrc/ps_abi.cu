@@ -33,6 +33,7 @@ struct ps_instance {
 struct ps_base {
     const ps_instance *inst;
     int K, cand_words, ck_words, ck_interval, ck_max;
+    int max_window;     // widest live ledger window the base needed (-1: unknown / unusable)
     uint32_t *ck;       // [ck_max][ck_words]
     uint32_t *cstep;    // [P][L]
     uint32_t *fstep;    // [P][m]
@@ -216,7 +217,11 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
     const int full = 5 * I->m;
-    int Ks[3] = {window_size(I), std::min(full, 4 * window_size(I)), full};
+    int K1 = window_size(I);
+    // with a recorded base, neighbours need about the base's window: size the first pass from it
+    if (B && B->inst == I && B->max_window >= 0 && !getenv("PS_WINDOW"))
+        K1 = std::min(full, std::max(8, B->max_window + 4));
+    int Ks[3] = {K1, std::min(full, 4 * K1), full};
     int npass = 1;
     if (Ks[0] < full) npass = Ks[1] < full ? 3 : 2;
     if (B && B->inst == I && p.chorders == nullptr && p.tcode == nullptr) attach_base(B, &p);
@@ -500,6 +505,7 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     if (!B) return fail(PS_ERR_NOMEM, "host allocation");
     B->inst = I;
     B->K = std::min(5 * I->m, 128);                 // recording window (checkpoints store it compactly)
+    B->max_window = -1;
     B->cand_words = words_per_candidate(I, B->K);
     {
         const int vw = I->v64 ? 2 : 1;
@@ -571,6 +577,11 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     }
     cudaError_t e = launch(I->v64, false, false, p, cfg, s, true);
     if (e != cudaSuccess) return cuda_fail(e, "base recording launch");
+    // the evaluation passes size their ledger window from the base's (one host read per record)
+    int32_t info[8];
+    PS_CUDA(cudaMemcpyAsync(info, B->info, sizeof info, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaStreamSynchronize(s));
+    B->max_window = info[0] > 0 ? info[4] : -1;
     return PS_OK;
 }
 
