@@ -93,6 +93,9 @@ struct EvalParams {
 
 constexpr int CK_REGW = 20;          // per-lane register words saved in a checkpoint
 constexpr uint32_t NEVER = 0xFFFFFFFFu;
+// An A[i][j] word no future event reads (B(i,j), W(i,j) and B(i-1,j) all committed).  Dead words
+// are canonical so that two simulations in the same live state compare equal.
+constexpr uint32_t A_DEAD = 0xFFFFFFFFu;
 
 template <typename V>
 __device__ __forceinline__ V ldv(const void *base, int idx) {
@@ -191,6 +194,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     unsigned long long tkey = KEY_ABSENT;      // cached best transfer key of this stage
     bool cdirty = false, tdirty = false, ovf = false;
     V base = 0, top = 0, peak = 0;
+    V segpk = 0;                               // REC: max usage folded since the last checkpoint
     int ws = 0, we = 0;
     int n_poff = 0, n_prel = 0, n_unrel = 0;   // pending offloads / reloads / offloaded not yet reloaded
     // earliest_fit cache, valid until the ledger changes; NO_R marks it empty (R >= -delta > NO_R)
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     uint32_t head = 0, nxt = 0;
     int cpos = 0;
     uint32_t chead = NO_CHAN, cnext = NO_CHAN;
+    int lastq = -1;     // last position of this stage's order that differs from the base's
+    int eoff = 0;       // base step = candidate step + eoff once the candidate's extra/missing transfers are done
 
     auto fetch = [&](int q) -> uint32_t {
         if (q >= L || !has_stage) return 0u;
@@ -216,6 +222,22 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         return __ldg(&p.chorders[((size_t)cand * p.G + chan_i) * p.chan_stride + q]);
     };
 
+    // The recorded base's offload bits of this stage, re-based to [MW] words (the incumbent's in
+    // move mode: the base is always the incumbent there).
+    auto base_word = [&](int w) -> uint32_t {
+        const int mwords = (P * m + 31) / 32;
+        const int gb = i * m + w * 32, q = gb >> 5, sh = gb & 31;
+        auto word = [&](int qq) -> uint32_t {
+            if (qq >= mwords) return 0u;
+            return MOVES ? incmask_s[qq] : __ldg(&p.base_mask[qq]);
+        };
+        uint32_t bits = word(q) >> sh;
+        if (sh) bits |= word(q + 1) << (32 - sh);
+        const int nb = m - w * 32;
+        if (nb < 32) bits &= (1u << nb) - 1u;
+        return bits;
+    };
+
     // Ledger window: the stage's merged breakpoints at or after the fold line, sorted by time, each
     // holding the usage AFTER it; slots [ws, we) of a 2K array, compacted when the end is reached.
     // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
@@ -223,6 +245,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         while (ws < we && (int)SW(o_wt + (ws)) < line) {
             V u = SV(o_wu + (ws));
             peak = u > peak ? u : peak;
+            if (REC) segpk = u > segpk ? u : segpk;
             base = u;
             ++ws;
         }
@@ -311,7 +334,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             fl = (int)(a >> 2);
             if (i < P - 1) {
                 uint32_t b = SW(o_A + ((i + 1) * m + j));
-                if ((b & 3u) != 2u) return;
+                if ((b & 3u) < 2u) return;               // 2: B committed, 3: and W too
                 fl = max(fl, (int)(b >> 2) + p.comm);
             }
             if ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) {
@@ -407,6 +430,38 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     };
     const int n_ck = (p.ck && !REC) ? p.base_info[0] : 0;
 
+    // Suffix sharing: every offload bit on which the candidate and the base differ
+    // is dead once that microbatch's B has committed on this stage.
+    auto diff_dead = [&]() -> bool {
+        for (int w = 0; w < MW; ++w)
+            for (uint32_t x = SW(o_offm + (w)) ^ base_word(w); x; x &= x - 1)
+                if ((SW(o_Ai + (w * 32 + __ffs(x) - 1)) & 3u) < 2u) return false;
+        return true;
+    };
+    // Is this candidate's live state before its current step that of the base before step c*C?
+    // Then both simulations continue identically and the base's outcome is the candidate's.
+    auto same_state = [&](int c) -> bool {
+        const uint32_t *src = p.ck + (size_t)c * p.ck_words;
+        bool eq = true;
+        const int o_skip = 2 * P * m, o_end = o_skip + P * MW;    // offm: its differences are dead
+        for (int k = lane; k < nz; k += 32)
+            if (k < o_skip || k >= o_end) eq = eq && SW(o_A + (k)) == src[k];
+        if (has_stage) {
+            const uint32_t *rg = src + ck_r + lane * CK_REGW;
+            eq = eq && pos == (int)rg[0] && sfree == (int)rg[1] && cfree == (int)rg[2] && we - ws == (int)rg[4] &&
+                 n_poff == (int)rg[5] && n_prel == (int)rg[6] && n_unrel == (int)rg[7] &&
+                 first_start == (int)rg[8] && (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
+                 (long long)top == *reinterpret_cast<const long long *>(rg + 14);
+            if (eq) {
+                const uint32_t *st = src + ck_t + i * p.ck_kc;
+                const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
+                for (int q = 0; q < we - ws && eq; ++q)
+                    eq = SW(o_wt + (ws + q)) == st[q] && SV(o_wu + (ws + q)) == su[q];
+            }
+        }
+        return __all_sync(0xffffffffu, eq);
+    };
+
     const long long n_items = p.work_list ? (long long)*p.work_count : p.N;
     for (long long item = slot; item < n_items; item += nslots) {
         cand = p.work_list ? (long long)p.work_list[item] : item;
@@ -468,6 +523,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
         // ---- prefix sharing: the first step whose inputs differ from the recorded base ----
         uint32_t div = 0u;
+        lastq = -1;
+        eoff = 0;
         if (n_ck > 0) {
             uint32_t d = NEVER;
             if (has_stage) {
@@ -476,27 +533,34 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     uint32_t c = p.cstep[i * L + q - 1];
                     return c == NEVER ? NEVER : c + 1u;
                 };
+                int nbase = 0;
                 if (MOVES) {
                     if (mv.stage == i) {
-                        if (mv.type == MOVE_SHIFT) d = after(min(mv.a, mv.b));
+                        if (mv.type == MOVE_SHIFT) { d = after(min(mv.a, mv.b)); lastq = max(mv.a, mv.b); }
                         else if (mv.type == MOVE_TOGGLE) d = p.fstep[i * m + mv.mb];
                     }
+                    for (int w = 0; w < MW; ++w) nbase += __popc(base_word(w));
                 } else {
                     const uint16_t *row = p.orders + ((size_t)cand * P + i) * p.stride;
                     const uint16_t *brow = p.base_orders + (size_t)i * p.stride;
                     int q = 0;
                     while (q < L && row[q] == brow[q]) ++q;
-                    if (q < L) d = after(q);
-                    const int mwords = (P * m + 31) / 32;
+                    if (q < L) {
+                        d = after(q);
+                        lastq = L - 1;
+                        while (lastq > q && row[lastq] == brow[lastq]) --lastq;
+                    }
                     for (int w = 0; w < MW; ++w) {
-                        const int gb = i * m + w * 32, qq = gb >> 5, sh = gb & 31;
-                        uint32_t bb = (qq < mwords ? p.base_mask[qq] : 0u) >> sh;
-                        if (sh && qq + 1 < mwords) bb |= p.base_mask[qq + 1] << (32 - sh);
-                        for (uint32_t x = (SW(o_offm + (w)) ^ bb) & (m - w * 32 < 32 ? (1u << (m - w * 32)) - 1u : ~0u); x; x &= x - 1)
+                        const uint32_t bb = base_word(w);
+                        nbase += __popc(bb);
+                        for (uint32_t x = SW(o_offm + (w)) ^ bb; x; x &= x - 1)
                             d = min(d, p.fstep[i * m + w * 32 + __ffs(x) - 1]);
                     }
                 }
+                eoff = nbase - cand_unrel;
             }
+            // the base runs two transfer events per offloaded activation the candidate does not have
+            eoff = 2 * __reduce_add_sync(0xffffffffu, eoff);
             div = __reduce_min_sync(0xffffffffu, d);
             if (div == NEVER) {
                 // identical to the base up to its end: its outcome is this candidate's
@@ -563,7 +627,18 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         // ================= simulate: one committed event per iteration ===================
         bool ck_full = false;
         int max_win = 0;
+        int conv_c = -1;
         for (;;) {
+            if (!REC && n_ck > 1) {
+                const int eb = ecount + eoff;
+                if (eb > 0 && ecount > (int)div && (eb & (p.ck_interval - 1)) == 0 && eb / p.ck_interval < n_ck) {
+                    const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead()));
+                    if (__all_sync(0xffffffffu, gate) && same_state(eb / p.ck_interval)) {
+                        conv_c = eb / p.ck_interval;
+                        break;
+                    }
+                }
+            }
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
             if (REC && (ecount & (p.ck_interval - 1)) == 0) {
                 const int c = ecount / p.ck_interval;
@@ -579,6 +654,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     we -= ws;
                     ws = 0;
                     save_regs(dst + ck_r + lane * CK_REGW);
+                    *reinterpret_cast<long long *>(dst + ck_r + lane * CK_REGW + 10) = (long long)segpk;
+                    segpk = 0;
                     ws = ws0;
                     we = we0;
                 } else {
@@ -622,6 +699,12 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                         if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
                     } else if (k == KIND_B) {
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 2u;
+                        SW(o_Xi + (j)) = 0u;                        // B(i, j) was its last reader
+                        if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 3u) SW(o_A + ((i + 1) * m + j)) = A_DEAD;
+                    } else {
+                        // W(i, j) is the last reader of A[i][j] unless B(i-1, j) is still to come
+                        const bool up_done = i == 0 || (SW(o_A + ((i - 1) * m + j)) & 3u) >= 2u;
+                        SW(o_Ai + (j)) = up_done ? A_DEAD : (SW(o_Ai + (j)) | 3u);
                     }
                     cdirty = true;
                     // reload keys read the ledger; a new request or explicit channel head may appear
@@ -665,6 +748,24 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
 
         // ================= finished or deadlocked =========================================
+        if (conv_c >= 0) {
+            // converged onto the base: its outcome, with this candidate's peak prefix
+            const uint32_t fl = (uint32_t)p.base_info[1];
+            if (p.peak && has_stage) {
+                const V sfx = (V)*reinterpret_cast<const long long *>(p.ck + (size_t)conv_c * p.ck_words + ck_r + lane * CK_REGW + 18);
+                p.peak[(size_t)cand * P + i] = fl == FLAG_FEASIBLE ? (long long)(peak > sfx ? peak : sfx) * p.unit : -1;
+            }
+            if (lane == 0) {
+                const long long span = p.base_res[0];
+                put_result(fl, span, (uint32_t)p.base_info[3]);
+                if (MOVES && p.best_key && span >= 0) {
+                    long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
+                    if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
+                }
+            }
+            __syncwarp();
+            continue;
+        }
         const unsigned rem = __ballot_sync(0xffffffffu, has_stage && pos < L);
         if (REC) {
             const bool unusable = __any_sync(0xffffffffu, ovf || ck_full);
@@ -676,6 +777,16 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, lo);
             }
             if (has_stage) p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
+            if (!unusable && has_stage) {
+                // S_c = max usage folded after checkpoint c (a converging candidate's peak suffix)
+                long long run = (long long)segpk;
+                for (int c = ecount / p.ck_interval; c >= 0; --c) {
+                    uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
+                    const long long sg = *reinterpret_cast<const long long *>(rg + 10);
+                    *reinterpret_cast<long long *>(rg + 18) = run;
+                    run = sg > run ? sg : run;
+                }
+            }
             if (lane == 0) {
                 p.base_info[0] = unusable ? -1 : ecount / p.ck_interval + 1;
                 p.base_info[4] = max_win;
