@@ -21,6 +21,7 @@ FLAG_MALFORMED = 4
 MAX_STAGES = 32
 MAX_MICROBATCHES = 4096
 BEST_NONE = (1 << 63) - 1
+BASE_CHECKPOINTS, BASE_CSTEP, BASE_FSTEP, BASE_INFO, BASE_RESULT = range(5)   # ps_base_read tables
 
 
 class NativeUnavailable(RuntimeError):
@@ -128,6 +129,7 @@ EXPORTS = {
     "ps_base_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "ps_base_destroy": (C.c_int, [C.c_void_p]),
     "ps_base_record": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_base_read": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_size_t)]),
 }
 
 _lib = None

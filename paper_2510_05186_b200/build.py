@@ -47,15 +47,18 @@ def _run(cmd):
     return r
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Build the library; `defines`/`out` produce an experiment variant (tools/kexp.py) elsewhere."""
+    lib = Path(out) if out else LIB
+    if not force and not defines and lib == LIB and not needs_build():
         return LIB
-    objdir = LIBDIR / "obj"
+    objdir = lib.parent / ("obj" if lib == LIB else "obj_" + lib.stem)
     objdir.mkdir(parents=True, exist_ok=True)
 
     def compile_one(src):
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", str(INCLUDE), "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", str(INCLUDE), "-c", str(CSRC / src),
+               "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = _run(cmd)
@@ -65,11 +68,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=Path(outs[0]) if outs else None))

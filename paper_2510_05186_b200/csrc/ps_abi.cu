@@ -41,6 +41,8 @@ struct ps_base {
     int64_t *res;       // [2 + P]
     uint16_t *orders;   // [P][stride]
     uint32_t *mask;     // [mask_words]
+    uint16_t *prev_orders;   // the previously recorded base (a re-recording resumes from its checkpoints)
+    uint32_t *prev_mask;
 };
 
 namespace {
@@ -226,11 +228,14 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
     if (Ks[0] < full) npass = Ks[1] < full ? 3 : 2;
     if (B && B->inst == I && p.chorders == nullptr && p.tcode == nullptr) attach_base(B, &p);
     // worklists, one per handoff between passes: [count][N candidate indices]
+    // followed by one dynamic-distribution counter per pass
     int32_t *lists = nullptr;
     const size_t list_words = (size_t)p.N + 1;
-    PS_CUDA(cudaMallocAsync((void **)&lists, 2 * list_words * sizeof(int32_t), s));
+    PS_CUDA(cudaMallocAsync((void **)&lists, (2 * list_words + 4) * sizeof(int32_t), s));
     PS_CUDA(cudaMemsetAsync(lists, 0, sizeof(int32_t), s));
     PS_CUDA(cudaMemsetAsync(lists + list_words, 0, sizeof(int32_t), s));
+    PS_CUDA(cudaMemsetAsync(lists + 2 * list_words, 0, 4 * sizeof(int32_t), s));
+    const bool dynamic = env_int("PS_DYNAMIC", 1) != 0;
     for (int k = 0; k < npass; ++k) {
         Plan pl;
         int rc = plan_pass(I, moves, Ks[k], p.N, &pl);
@@ -245,6 +250,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.work_list = in ? in + 1 : nullptr;
         q.ovf_count = out;
         q.ovf_list = out ? out + 1 : nullptr;
+        q.work_next = dynamic ? lists + 2 * list_words + k : nullptr;
         uint32_t *scratch = nullptr;
         if (pl.scratch_bytes) PS_CUDA(cudaMallocAsync((void **)&scratch, pl.scratch_bytes, s));
         q.gstate = scratch;
@@ -523,6 +529,8 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->res, (size_t)(2 + I->P) * sizeof(int64_t));
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->orders, (size_t)I->P * I->stride * 2);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->mask, (size_t)I->mask_words * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_orders, (size_t)I->P * I->stride * 2);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_mask, (size_t)I->mask_words * 4);
     if (e == cudaSuccess) e = cudaMemset(B->info, 0xFF, 8 * sizeof(int32_t));   // -1: nothing recorded
     if (e != cudaSuccess) {
         ps_base_destroy(B);
@@ -542,6 +550,8 @@ int ps_base_destroy(ps_base *B) {
     cudaFree(B->res);
     cudaFree(B->orders);
     cudaFree(B->mask);
+    cudaFree(B->prev_orders);
+    cudaFree(B->prev_mask);
     delete B;
     return PS_OK;
 }
@@ -552,10 +562,19 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     DeviceGuard guard(I->device);
     if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
     cudaStream_t s = (cudaStream_t)stream;
+    // A usable previous recording is kept: the new base replays it up to their first difference
+    // (its checkpoints, cstep and fstep entries before that point are the new base's too).
+    const bool resume = B->max_window >= 0 && env_int("PS_REC_RESUME", 1) != 0;
+    if (resume) {
+        PS_CUDA(cudaMemcpyAsync(B->prev_orders, B->orders, (size_t)I->P * I->stride * 2, cudaMemcpyDeviceToDevice, s));
+        PS_CUDA(cudaMemcpyAsync(B->prev_mask, B->mask, (size_t)I->mask_words * 4, cudaMemcpyDeviceToDevice, s));
+    }
     PS_CUDA(cudaMemcpyAsync(B->orders, orders, (size_t)I->P * I->stride * 2, cudaMemcpyDeviceToDevice, s));
     PS_CUDA(cudaMemcpyAsync(B->mask, mask, (size_t)I->mask_words * 4, cudaMemcpyDeviceToDevice, s));
-    PS_CUDA(cudaMemsetAsync(B->cstep, 0xFF, (size_t)I->P * I->L * 4, s));
-    PS_CUDA(cudaMemsetAsync(B->fstep, 0xFF, (size_t)I->P * I->m * 4, s));
+    if (!resume) {
+        PS_CUDA(cudaMemsetAsync(B->cstep, 0xFF, (size_t)I->P * I->L * 4, s));
+        PS_CUDA(cudaMemsetAsync(B->fstep, 0xFF, (size_t)I->P * I->m * 4, s));
+    }
     EvalParams p;
     memset(&p, 0, sizeof p);
     fill_instance(I, &p);
@@ -566,6 +585,11 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     p.cand_words = B->cand_words;
     p.inc_words = 0;
     attach_base(B, &p);
+    if (resume) {
+        p.base_orders = B->prev_orders;
+        p.base_mask = B->prev_mask;
+        p.rec_prev = 1;
+    }
     LaunchCfg cfg;
     cfg.grid = 1;
     cfg.block = 32;
@@ -582,6 +606,29 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     PS_CUDA(cudaMemcpyAsync(info, B->info, sizeof info, cudaMemcpyDeviceToHost, s));
     PS_CUDA(cudaStreamSynchronize(s));
     B->max_window = info[0] > 0 ? info[4] : -1;
+    return PS_OK;
+}
+
+int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
+    if (!B || !bytes) return fail(PS_ERR_INVALID, "null argument");
+    const ps_instance *I = B->inst;
+    const void *src = nullptr;
+    size_t n = 0;
+    switch (what) {
+        case PS_BASE_CHECKPOINTS: src = B->ck; n = (size_t)B->ck_max * B->ck_words * 4; break;
+        case PS_BASE_CSTEP: src = B->cstep; n = (size_t)I->P * I->L * 4; break;
+        case PS_BASE_FSTEP: src = B->fstep; n = (size_t)I->P * I->m * 4; break;
+        case PS_BASE_INFO: src = B->info; n = 8 * sizeof(int32_t); break;
+        case PS_BASE_RESULT: src = B->res; n = (size_t)(2 + I->P) * sizeof(int64_t); break;
+        default: return fail(PS_ERR_INVALID, "unknown base table %d", what);
+    }
+    if (!host) { *bytes = n; return PS_OK; }
+    if (*bytes < n) return fail(PS_ERR_RANGE, "buffer of %zu bytes < %zu", *bytes, n);
+    *bytes = n;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    PS_CUDA(cudaDeviceSynchronize());
+    PS_CUDA(cudaMemcpy(host, src, n, cudaMemcpyDeviceToHost));
     return PS_OK;
 }
 

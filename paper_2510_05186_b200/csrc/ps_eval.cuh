@@ -70,6 +70,7 @@ struct EvalParams {
     // overflow hand-off between the shared-memory and the global-state variant
     int32_t *ovf_list;
     int32_t *ovf_count;
+    int32_t *work_next;      // dynamic candidate distribution (NULL: static grid stride)
     const int32_t *work_list;
     const int32_t *work_count;
     // per-candidate state
@@ -87,8 +88,9 @@ struct EvalParams {
     uint32_t *fstep;         // [P][m] step at which the base commits F(i, j)
     int32_t *base_info;      // [0] checkpoints (-1 unusable) [1] flags [2] events [3] blocked [4] max window
     int64_t *base_res;       // [0] makespan [1] bubble bits [2 .. 2+P) peaks
-    const uint16_t *base_orders;   // [P][stride] (materialised candidates)
+    const uint16_t *base_orders;   // [P][stride] (materialised candidates; REC: the previous base)
     const uint32_t *base_mask;     // [mask_words]
+    int rec_prev;                  // REC: resume from the previous base's checkpoints
 };
 
 constexpr int CK_REGW = 20;          // per-lane register words saved in a checkpoint
@@ -429,6 +431,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         peak = (V)*reinterpret_cast<const long long *>(rg + 16);
     };
     const int n_ck = (p.ck && !REC) ? p.base_info[0] : 0;
+    // Checkpoints to resume from: the base's for a candidate; for a re-recording (REC with
+    // rec_prev) those of the previous base, whose prefix the new one shares up to their divergence.
+    const int n_src = REC ? (p.rec_prev ? p.base_info[0] : 0) : n_ck;
 
     // Suffix sharing: every offload bit on which the candidate and the base differ
     // is dead once that microbatch's B has committed on this stage.
@@ -443,27 +448,38 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto same_state = [&](int c) -> bool {
         const uint32_t *src = p.ck + (size_t)c * p.ck_words;
         bool eq = true;
-        const int o_skip = 2 * P * m, o_end = o_skip + P * MW;    // offm: its differences are dead
-        for (int k = lane; k < nz; k += 32)
-            if (k < o_skip || k >= o_end) eq = eq && SW(o_A + (k)) == src[k];
+        // the per-stage scalars first: they tell a still-perturbed candidate apart cheaply
         if (has_stage) {
             const uint32_t *rg = src + ck_r + lane * CK_REGW;
-            eq = eq && pos == (int)rg[0] && sfree == (int)rg[1] && cfree == (int)rg[2] && we - ws == (int)rg[4] &&
+            eq = pos == (int)rg[0] && sfree == (int)rg[1] && cfree == (int)rg[2] && we - ws == (int)rg[4] &&
                  n_poff == (int)rg[5] && n_prel == (int)rg[6] && n_unrel == (int)rg[7] &&
                  first_start == (int)rg[8] && (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
                  (long long)top == *reinterpret_cast<const long long *>(rg + 14);
-            if (eq) {
-                const uint32_t *st = src + ck_t + i * p.ck_kc;
-                const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
-                for (int q = 0; q < we - ws && eq; ++q)
-                    eq = SW(o_wt + (ws + q)) == st[q] && SV(o_wu + (ws + q)) == su[q];
-            }
+        }
+        if (!__all_sync(0xffffffffu, eq)) return false;
+        const int o_skip = 2 * P * m, o_end = o_skip + P * MW;    // offm: its differences are dead
+        for (int k = lane; k < nz; k += 32)
+            if (k < o_skip || k >= o_end) eq = eq && SW(o_A + (k)) == src[k];
+        if (has_stage && eq) {
+            const uint32_t *st = src + ck_t + i * p.ck_kc;
+            const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
+            for (int q = 0; q < we - ws && eq; ++q)
+                eq = SW(o_wt + (ws + q)) == st[q] && SV(o_wu + (ws + q)) == su[q];
         }
         return __all_sync(0xffffffffu, eq);
     };
 
     const long long n_items = p.work_list ? (long long)*p.work_count : p.N;
-    for (long long item = slot; item < n_items; item += nslots) {
+    // Candidates cost from tens to thousands of events: after the first, each warp takes the next
+    // unclaimed one (one atomic per candidate) so no SM idles behind a few long simulations.
+    long long item = slot;
+    auto next_item = [&]() -> long long {
+        if (!p.work_next) return item + nslots;
+        int v = 0;
+        if (lane == 0) v = atomicAdd(p.work_next, 1);
+        return nslots + (long long)__shfl_sync(0xffffffffu, v, 0);
+    };
+    for (; item < n_items; item = next_item()) {
         cand = p.work_list ? (long long)p.work_list[item] : item;
         // ================= initialise ======================================================
         for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = 0u;
@@ -525,7 +541,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         uint32_t div = 0u;
         lastq = -1;
         eoff = 0;
-        if (n_ck > 0) {
+        if (n_src > 0) {
             uint32_t d = NEVER;
             if (has_stage) {
                 auto after = [&](int q) -> uint32_t {   // first step at which stage i's head is position q
@@ -562,6 +578,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             // the base runs two transfer events per offloaded activation the candidate does not have
             eoff = 2 * __reduce_add_sync(0xffffffffu, eoff);
             div = __reduce_min_sync(0xffffffffu, d);
+            if (REC && div == NEVER) div = 0u;        // same base again: record it afresh
             if (div == NEVER) {
                 // identical to the base up to its end: its outcome is this candidate's
                 if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = p.base_res[2 + i];
@@ -578,7 +595,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 continue;
             }
         }
-        const int ck_idx = n_ck > 0 ? min((int)(div / (uint32_t)p.ck_interval), n_ck - 1) : 0;
+        const int ck_idx = n_src > 0 ? min((int)(div / (uint32_t)p.ck_interval), n_src - 1) : 0;
         if (ck_idx > 0) {
             const uint32_t *src = p.ck + (size_t)ck_idx * p.ck_words;
             load_regs(src + ck_r + lane * CK_REGW);
@@ -605,6 +622,16 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 for (int w = 0; w < MW; ++w) nb += __popc(SW(o_offm + (w)));
                 n_unrel += cand_unrel - nb;
                 build_mask(false);
+                if (REC) {
+                    // the kept checkpoints become the new base's: its offload bits, and the
+                    // outstanding-transfer count that goes with them (the suffix-sharing compare
+                    // reads both)
+                    for (int c = 0; c <= ck_idx; ++c) {
+                        uint32_t *dst = p.ck + (size_t)c * p.ck_words;
+                        for (int w = 0; w < MW; ++w) dst[2 * P * m + i * MW + w] = SW(o_offm + (w));
+                        dst[ck_r + lane * CK_REGW + 7] += (uint32_t)(cand_unrel - nb);
+                    }
+                }
             }
             ecount = ck_idx * p.ck_interval;
             ecount0 = ecount;
@@ -626,7 +653,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
 
         // ================= simulate: one committed event per iteration ===================
         bool ck_full = false;
-        int max_win = 0;
+        // a resumed recording starts from the previous base's widest window up to its checkpoint
+        int max_win = REC && ecount0 > 0 ? (int)p.ck[(size_t)(ecount0 / p.ck_interval) * p.ck_words + ck_r + 9] : 0;
         int conv_c = -1;
         for (;;) {
             if (!REC && n_ck > 1) {
@@ -640,7 +668,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 }
             }
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
-            if (REC && (ecount & (p.ck_interval - 1)) == 0) {
+            // (a re-recording keeps the previous base's checkpoint it resumed from: same state)
+            if (REC && (ecount & (p.ck_interval - 1)) == 0 && !(ecount == ecount0 && ecount0 > 0)) {
                 const int c = ecount / p.ck_interval;
                 if (c < p.ck_max) {
                     uint32_t *dst = p.ck + (size_t)c * p.ck_words;
@@ -655,6 +684,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     ws = 0;
                     save_regs(dst + ck_r + lane * CK_REGW);
                     *reinterpret_cast<long long *>(dst + ck_r + lane * CK_REGW + 10) = (long long)segpk;
+                    dst[ck_r + lane * CK_REGW + 9] = (uint32_t)max_win;     // widest window so far
                     segpk = 0;
                     ws = ws0;
                     we = we0;
@@ -777,6 +807,13 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, lo);
             }
             if (has_stage) p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
+            if (has_stage && rem != 0u) {
+                // deadlocked base: what it never committed is NEVER (a resumed recording would
+                // otherwise keep the previous base's steps there)
+                for (int q = pos; q < L; ++q) p.cstep[i * L + q] = NEVER;
+                for (int j = 0; j < m; ++j)
+                    if ((SW(o_Ai + (j)) & 3u) == 0u) p.fstep[i * m + j] = NEVER;
+            }
             if (!unusable && has_stage) {
                 // S_c = max usage folded after checkpoint c (a converging candidate's peak suffix)
                 long long run = (long long)segpk;

@@ -145,6 +145,14 @@ class Base:
         N.check(self.di.lib.ps_base_record(self.handle, C.c_void_p(orders.data_ptr()),
                                            C.c_void_p(mask.data_ptr()), self.di._stream(stream)))
 
+    def read(self, what: int):
+        """One recorded table (N.BASE_*) as raw bytes (synchronises the device)."""
+        n = C.c_size_t(0)
+        N.check(self.di.lib.ps_base_read(self.handle, what, None, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        N.check(self.di.lib.ps_base_read(self.handle, what, buf, C.byref(n)))
+        return buf.raw
+
 
 _CACHE: dict = {}
 _CACHE_LOCK = threading.Lock()

@@ -167,6 +167,27 @@ def test_prefix_sharing_is_exact(cuda_ok, cfg):
     _eval_both(ls.di, o, mk, bad)
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_rerecorded_base_is_exact(cuda_ok, cfg):
+    """A base re-recorded over a previous one (it resumes from the previous checkpoints up to their
+    first difference) shares exactly: feasible and deadlocking bases in turn."""
+    from paper_2510_05186_b200.engine import Base
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    n = 1024
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT, share_prefix=True))
+    o, mk = ls.materialize(0, n, 1)
+    flags = ls.di.evaluate(o, mk, peak=False).flags.cpu().numpy()
+    feas = [int(x) for x in np.nonzero(flags & 1)[0][:3]]
+    dead = [int(x) for x in np.nonzero(flags & 2)[0][:2]]
+    assert len(feas) == 3 and len(dead) == 2
+    rb = Base(ls.di)
+    rb.record(ls.inc_orders, ls.inc_mask)
+    for idx in (feas[0], dead[0], feas[1], dead[1], feas[2]):
+        rb.record(o[idx], mk[idx])
+        _eval_both(ls.di, o, mk, rb)
+
+
 def test_host_buffer_path_matches_device_path(cuda_ok):
     """ps_eval_batch_host (chunked, copies overlapped) == ps_eval_batch on the same candidates."""
     import torch
