@@ -38,7 +38,7 @@ struct ps_base {
     uint32_t *cstep;    // [P][L]
     uint32_t *fstep;    // [P][m]
     int32_t *info;      // [4]
-    int64_t *res;       // [2 + P]
+    int64_t *res;       // [2 + 3P]
     uint16_t *orders;   // [P][stride]
     uint32_t *mask;     // [mask_words]
     uint16_t *prev_orders;   // the previously recorded base (a re-recording resumes from its checkpoints)
@@ -526,7 +526,7 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->cstep, (size_t)I->P * I->L * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->fstep, (size_t)I->P * I->m * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->info, 8 * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc((void **)&B->res, (size_t)(2 + I->P) * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMalloc((void **)&B->res, (size_t)(2 + 3 * I->P) * sizeof(int64_t));
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->orders, (size_t)I->P * I->stride * 2);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->mask, (size_t)I->mask_words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_orders, (size_t)I->P * I->stride * 2);
@@ -619,7 +619,7 @@ int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
         case PS_BASE_CSTEP: src = B->cstep; n = (size_t)I->P * I->L * 4; break;
         case PS_BASE_FSTEP: src = B->fstep; n = (size_t)I->P * I->m * 4; break;
         case PS_BASE_INFO: src = B->info; n = 8 * sizeof(int32_t); break;
-        case PS_BASE_RESULT: src = B->res; n = (size_t)(2 + I->P) * sizeof(int64_t); break;
+        case PS_BASE_RESULT: src = B->res; n = (size_t)(2 + 3 * I->P) * sizeof(int64_t); break;
         default: return fail(PS_ERR_INVALID, "unknown base table %d", what);
     }
     if (!host) { *bytes = n; return PS_OK; }

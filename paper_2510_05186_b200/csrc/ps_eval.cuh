@@ -87,7 +87,8 @@ struct EvalParams {
     uint32_t *cstep;         // [P][L] step at which the base commits stage i's q-th op (~0 = never)
     uint32_t *fstep;         // [P][m] step at which the base commits F(i, j)
     int32_t *base_info;      // [0] checkpoints (-1 unusable) [1] flags [2] events [3] blocked [4] max window
-    int64_t *base_res;       // [0] makespan [1] bubble bits [2 .. 2+P) peaks
+    int64_t *base_res;       // [0] makespan [1] bubble bits [2, 2+P) peaks [2+P, 2+2P) final free
+                             // times [2+2P, 2+3P) first starts
     const uint16_t *base_orders;   // [P][stride] (materialised candidates; REC: the previous base)
     const uint32_t *base_mask;     // [mask_words]
     int rec_prev;                  // REC: resume from the previous base's checkpoints
@@ -443,29 +444,44 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 if ((SW(o_Ai + (w * 32 + __ffs(x) - 1)) & 3u) < 2u) return false;
         return true;
     };
-    // Is this candidate's live state before its current step that of the base before step c*C?
-    // Then both simulations continue identically and the base's outcome is the candidate's.
+    // Is this candidate's live state before its current step that of the base before step c*C,
+    // up to one time shift `delta` of every live time (stage and channel free times, live F/B and
+    // transfer end times, ledger breakpoints; usages, positions and pending sets equal)?  The
+    // scheduler is translation invariant on such states — every start is a max of live times plus
+    // constants, every commit adds a constant, the fold line moves with them — so the candidate
+    // continues as the base does, `delta` later.
+    int conv_delta = 0;
     auto same_state = [&](int c) -> bool {
         const uint32_t *src = p.ck + (size_t)c * p.ck_words;
+        const uint32_t *rg = src + ck_r + lane * CK_REGW;
         bool eq = true;
+        const int d = __shfl_sync(0xffffffffu, sfree - (int)rg[1], 0);
         // the per-stage scalars first: they tell a still-perturbed candidate apart cheaply
         if (has_stage) {
-            const uint32_t *rg = src + ck_r + lane * CK_REGW;
-            eq = pos == (int)rg[0] && sfree == (int)rg[1] && cfree == (int)rg[2] && we - ws == (int)rg[4] &&
+            // a channel that has carried nothing yet (free time 0 on both) constrains nothing
+            eq = pos == (int)rg[0] && sfree - (int)rg[1] == d &&
+                 (cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u)) && we - ws == (int)rg[4] &&
                  n_poff == (int)rg[5] && n_prel == (int)rg[6] && n_unrel == (int)rg[7] &&
-                 first_start == (int)rg[8] && (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
+                 (first_start == INT_MAX) == ((int)rg[8] == INT_MAX) &&
+                 (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
                  (long long)top == *reinterpret_cast<const long long *>(rg + 14);
         }
         if (!__all_sync(0xffffffffu, eq)) return false;
-        const int o_skip = 2 * P * m, o_end = o_skip + P * MW;    // offm: its differences are dead
-        for (int k = lane; k < nz; k += 32)
-            if (k < o_skip || k >= o_end) eq = eq && SW(o_A + (k)) == src[k];
+        // end-time words (time << 2 | state): equal, or both live with times delta apart
+        const uint32_t d4 = (uint32_t)d << 2;
+        for (int k = lane; k < 2 * P * m; k += 32) {
+            const uint32_t cw = SW(o_A + (k)), bw = src[k];
+            eq = eq && (cw == bw || ((cw & 3u) != 0u && cw != A_DEAD && bw != A_DEAD && cw - bw == d4));
+        }
+        for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
+            eq = eq && SW(o_A + (k)) == src[k];
         if (has_stage && eq) {
             const uint32_t *st = src + ck_t + i * p.ck_kc;
             const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
             for (int q = 0; q < we - ws && eq; ++q)
-                eq = SW(o_wt + (ws + q)) == st[q] && SV(o_wu + (ws + q)) == su[q];
+                eq = (int)SW(o_wt + (ws + q)) - (int)st[q] == d && SV(o_wu + (ws + q)) == su[q];
         }
+        conv_delta = d;
         return __all_sync(0xffffffffu, eq);
     };
 
@@ -785,8 +801,17 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 const V sfx = (V)*reinterpret_cast<const long long *>(p.ck + (size_t)conv_c * p.ck_words + ck_r + lane * CK_REGW + 18);
                 p.peak[(size_t)cand * P + i] = fl == FLAG_FEASIBLE ? (long long)(peak > sfx ? peak : sfx) * p.unit : -1;
             }
+            // the base's final free and first-start times, delta later (a stage that had started
+            // keeps its own first start)
+            long long span = -1;
+            if (fl == FLAG_FEASIBLE) {
+                const int hi = has_stage ? (int)p.base_res[2 + P + i] + conv_delta : 0;
+                const int fs = !has_stage ? INT_MAX
+                             : first_start != INT_MAX ? first_start : (int)p.base_res[2 + 2 * P + i] + conv_delta;
+                if (p.post) span = __reduce_max_sync(0xffffffffu, has_stage ? hi - fs : 0);
+                else span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, fs);
+            }
             if (lane == 0) {
-                const long long span = p.base_res[0];
                 put_result(fl, span, (uint32_t)p.base_info[3]);
                 if (MOVES && p.best_key && span >= 0) {
                     long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
@@ -806,7 +831,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 int lo = p.post ? 0 : (has_stage ? first_start : INT_MAX);
                 span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, lo);
             }
-            if (has_stage) p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
+            if (has_stage) {
+                p.base_res[2 + i] = rem == 0u ? (long long)peak * p.unit : -1;
+                p.base_res[2 + P + i] = sfree;            // final free time and first start: a candidate
+                p.base_res[2 + 2 * P + i] = first_start;  // converging with a time shift rebuilds its span
+            }
             if (has_stage && rem != 0u) {
                 // deadlocked base: what it never committed is NEVER (a resumed recording would
                 // otherwise keep the previous base's steps there)
