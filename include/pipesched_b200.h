@@ -147,8 +147,12 @@ int ps_base_destroy(ps_base *base);
 int ps_base_record(ps_base *base, const uint16_t *orders, const uint32_t *mask, void *stream);
 /* Inspection (tests, diagnostics): copy one recorded table to host memory after synchronising.
    what: PS_BASE_CHECKPOINTS [ck_max][ck_words] u32, PS_BASE_CSTEP [P][3m] u32, PS_BASE_FSTEP [P][m] u32,
-   PS_BASE_INFO i32[8], PS_BASE_RESULT i64[2 + 3P].  *bytes in: capacity, out: size of the table. */
-enum { PS_BASE_CHECKPOINTS = 0, PS_BASE_CSTEP = 1, PS_BASE_FSTEP = 2, PS_BASE_INFO = 3, PS_BASE_RESULT = 4 };
+   PS_BASE_INFO i32[8], PS_BASE_RESULT i64[2 + 3P], PS_BASE_LAYOUT i32[8] (ck_words, ck_max,
+   ck_interval, window capacity, then the word offsets of the breakpoint times, their usages and the
+   per-lane scalars inside a checkpoint, and the scalar words per lane).
+   *bytes in: capacity, out: size of the table. */
+enum { PS_BASE_CHECKPOINTS = 0, PS_BASE_CSTEP = 1, PS_BASE_FSTEP = 2, PS_BASE_INFO = 3, PS_BASE_RESULT = 4,
+       PS_BASE_LAYOUT = 5 };
 int ps_base_read(const ps_base *base, int what, void *host, size_t *bytes);
 
 /* Evaluate N candidates (device buffers) on `stream` (a cudaStream_t, NULL = legacy default). */

@@ -21,7 +21,7 @@ FLAG_MALFORMED = 4
 MAX_STAGES = 32
 MAX_MICROBATCHES = 4096
 BEST_NONE = (1 << 63) - 1
-BASE_CHECKPOINTS, BASE_CSTEP, BASE_FSTEP, BASE_INFO, BASE_RESULT = range(5)   # ps_base_read tables
+BASE_CHECKPOINTS, BASE_CSTEP, BASE_FSTEP, BASE_INFO, BASE_RESULT, BASE_LAYOUT = range(6)   # ps_base_read
 
 
 class NativeUnavailable(RuntimeError):

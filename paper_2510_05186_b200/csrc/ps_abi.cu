@@ -325,6 +325,58 @@ __global__ void apply_move_kernel(MoveCtx c, ps_move_params mp, uint64_t round, 
     }
 }
 
+// A re-recording that converged onto the previous base at checkpoint c0 with time shift dl
+// (base info[5], info[6]): every later checkpoint is the previous base's with each live time
+// moved by dl — F/B/transfer end words, ledger breakpoints, stage and used-channel free times —
+// the new base's offload bits and first starts, and the new peak prefix.  One block per
+// checkpoint.
+struct RecShift {
+    int P, m, MW, mask_words, ck_words, ck_kc, ck_t, ck_r, ck_max;
+    uint32_t *ck;
+    const int32_t *info;
+    const uint32_t *mask;
+};
+
+__global__ void rec_shift_kernel(RecShift r) {
+    const int c0 = r.info[5];
+    const int c = blockIdx.x;
+    if (c0 < 0 || c <= c0 || c >= r.info[0]) return;
+    const int dl = r.info[6];
+    uint32_t *ck = r.ck + (size_t)c * r.ck_words;
+    const uint32_t d4 = (uint32_t)dl << 2;
+    for (int k = threadIdx.x; k < 2 * r.P * r.m; k += blockDim.x) {
+        const uint32_t w = ck[k];
+        if ((w >> 2) && w != ps::A_DEAD) ck[k] = w + d4;      // words that carry a time
+    }
+    for (int k = threadIdx.x; k < r.P * r.MW; k += blockDim.x) {
+        const int s = k / r.MW, w = k % r.MW;
+        const int gb = s * r.m + w * 32, q = gb >> 5, sh = gb & 31;
+        uint32_t bits = (q < r.mask_words ? r.mask[q] : 0u) >> sh;
+        if (sh && q + 1 < r.mask_words) bits |= r.mask[q + 1] << (32 - sh);
+        const int nb = r.m - w * 32;
+        if (nb < 32) bits &= (1u << nb) - 1u;
+        ck[2 * r.P * r.m + k] = bits;
+    }
+    const uint32_t *rg0 = r.ck + (size_t)c0 * r.ck_words + r.ck_r;
+    for (int s = threadIdx.x; s < r.P; s += blockDim.x) {
+        uint32_t *rg = ck + r.ck_r + s * ps::CK_REGW;
+        const int count = (int)rg[4];
+        for (int q = 0; q < count; ++q) ck[r.ck_t + s * r.ck_kc + q] += (uint32_t)dl;
+        rg[1] += (uint32_t)dl;
+        if (rg[2]) rg[2] += (uint32_t)dl;
+        const int fs0 = (int)rg0[s * ps::CK_REGW + 8];
+        if (fs0 != INT_MAX) rg[8] = (uint32_t)fs0;
+        else if ((int)rg[8] != INT_MAX) rg[8] += (uint32_t)dl;
+        rg[20] -= (uint32_t)r.info[7];          // event step: the transfers differ by eoff
+        long long pk = *reinterpret_cast<const long long *>(rg0 + s * ps::CK_REGW + 16);
+        for (int k = c0 + 1; k <= c; ++k) {
+            const long long sg = *reinterpret_cast<const long long *>(r.ck + (size_t)k * r.ck_words + r.ck_r + s * ps::CK_REGW + 10);
+            pk = sg > pk ? sg : pk;
+        }
+        *reinterpret_cast<long long *>(rg + 16) = pk;
+    }
+}
+
 // Independent IADD3/LOP3/IMAD chains: the INT32 issue ceiling of the roofline.
 __global__ void int32_probe_kernel(int64_t iters, uint32_t seed, unsigned long long *lane_ops, uint32_t *sink) {
     uint32_t a0 = threadIdx.x ^ seed, a1 = a0 * 3u, a2 = a0 + 7u, a3 = a0 ^ 0x55u;
@@ -520,8 +572,9 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
         const int ck_u = (ck_t + I->P * B->K + 1) & ~1;
         B->ck_words = ck_u + I->P * B->K * vw + 32 * CK_REGW;
     }
-    B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 32))));
-    B->ck_max = 5 * I->P * I->m / B->ck_interval + 2;
+    // checkpoints every ck_interval compute events (3Pm per candidate)
+    B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 16))));
+    B->ck_max = 3 * I->P * I->m / B->ck_interval + 2;
     cudaError_t e = cudaMalloc((void **)&B->ck, (size_t)B->ck_max * B->ck_words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->cstep, (size_t)I->P * I->L * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->fstep, (size_t)I->P * I->m * 4);
@@ -601,6 +654,18 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     }
     cudaError_t e = launch(I->v64, false, false, p, cfg, s, true);
     if (e != cudaSuccess) return cuda_fail(e, "base recording launch");
+    if (resume) {
+        RecShift r;
+        r.P = I->P; r.m = I->m; r.MW = I->MW; r.mask_words = I->mask_words;
+        r.ck_words = B->ck_words; r.ck_kc = B->K; r.ck_max = B->ck_max;
+        const int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
+        r.ck_t = (nz + 1) & ~1;
+        const int ck_u = (r.ck_t + I->P * B->K + 1) & ~1;
+        r.ck_r = ck_u + I->P * B->K * (I->v64 ? 2 : 1);
+        r.ck = B->ck; r.info = B->info; r.mask = B->mask;
+        rec_shift_kernel<<<B->ck_max, 128, 0, s>>>(r);
+        PS_CUDA(cudaGetLastError());
+    }
     // the evaluation passes size their ledger window from the base's (one host read per record)
     int32_t info[8];
     PS_CUDA(cudaMemcpyAsync(info, B->info, sizeof info, cudaMemcpyDeviceToHost, s));
@@ -620,6 +685,18 @@ int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
         case PS_BASE_FSTEP: src = B->fstep; n = (size_t)I->P * I->m * 4; break;
         case PS_BASE_INFO: src = B->info; n = 8 * sizeof(int32_t); break;
         case PS_BASE_RESULT: src = B->res; n = (size_t)(2 + 3 * I->P) * sizeof(int64_t); break;
+        case PS_BASE_LAYOUT: {
+            const int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
+            const int ck_t = (nz + 1) & ~1;
+            const int ck_u = (ck_t + I->P * B->K + 1) & ~1;
+            const int32_t lay[8] = {B->ck_words, B->ck_max, B->ck_interval, B->K, ck_t, ck_u,
+                                    ck_u + I->P * B->K * (I->v64 ? 2 : 1), CK_REGW};
+            if (!host) { *bytes = sizeof lay; return PS_OK; }
+            if (*bytes < sizeof lay) return fail(PS_ERR_RANGE, "buffer too small");
+            memcpy(host, lay, sizeof lay);
+            *bytes = sizeof lay;
+            return PS_OK;
+        }
         default: return fail(PS_ERR_INVALID, "unknown base table %d", what);
     }
     if (!host) { *bytes = n; return PS_OK; }

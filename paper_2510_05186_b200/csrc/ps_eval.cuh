@@ -94,7 +94,7 @@ struct EvalParams {
     int rec_prev;                  // REC: resume from the previous base's checkpoints
 };
 
-constexpr int CK_REGW = 20;          // per-lane register words saved in a checkpoint
+constexpr int CK_REGW = 24;          // per-lane register words saved in a checkpoint
 constexpr uint32_t NEVER = 0xFFFFFFFFu;
 // An A[i][j] word no future event reads (B(i,j), W(i,j) and B(i-1,j) all committed).  Dead words
 // are canonical so that two simulations in the same live state compare equal.
@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     int tauF = 0, tauG = 0;
     int first_start = INT_MAX;      // start of the stage's first op (always an F; its last op is always a W)
     int ecount = 0, ecount0 = 0;             // events committed / restored from a checkpoint
+    int cc = 0;                              // compute events committed (checkpoints count these)
     uint32_t head = 0, nxt = 0;
     int cpos = 0;
     uint32_t chead = NO_CHAN, cnext = NO_CHAN;
@@ -409,11 +410,17 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (p.blocked) p.blocked[cand] = blocked_mask;
     };
 
-    // Checkpoint (state before step c*C), independent of the evaluating pass's window K:
+    // Checkpoint c: the state before the base commits its compute event number c*C (compute
+    // events, not all events: a candidate with other offload bits runs other transfers but the
+    // same 3Pm computes, so its states line up with the base's).  Independent of the evaluating
+    // pass's window K:
     //   [0, nz)               A, X, offm, poff, prel
     //   [ck_t, ck_t + P*KC)   each stage's live breakpoint times, compacted to slot 0
     //   [ck_u, ck_u + P*KC*VW) their usages
-    //   [ck_r, ck_r + 32*CK_REGW) every lane's scalars (window as ws = 0, we = count)
+    //   [ck_r, ck_r + 32*CK_REGW) every lane's scalars (window as ws = 0, we = count): 0-8 see
+    //                         save_regs, 9 widest window so far, 10-11 peak folded since the
+    //                         previous checkpoint, 12-17 base/top/peak, 18-19 peak folded after
+    //                         this checkpoint (S_c), 20 event step
     const int ck_t = (nz + 1) & ~1;
     const int ck_u = (ck_t + P * p.ck_kc + 1) & ~1;
     const int ck_r = ck_u + P * p.ck_kc * VW;
@@ -467,11 +474,13 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                  (long long)top == *reinterpret_cast<const long long *>(rg + 14);
         }
         if (!__all_sync(0xffffffffu, eq)) return false;
-        // end-time words (time << 2 | state): equal, or both live with times delta apart
+        // end-time words (time << 2 | state): a word that still carries a time (> 0) must be the
+        // base's moved by delta; state-only words (time 0, dead) must be equal
         const uint32_t d4 = (uint32_t)d << 2;
         for (int k = lane; k < 2 * P * m; k += 32) {
             const uint32_t cw = SW(o_A + (k)), bw = src[k];
-            eq = eq && (cw == bw || ((cw & 3u) != 0u && cw != A_DEAD && bw != A_DEAD && cw - bw == d4));
+            const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
+            eq = eq && (timed_c == timed_b) && (timed_c ? cw - bw == d4 : cw == bw);
         }
         for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
             eq = eq && SW(o_A + (k)) == src[k];
@@ -560,11 +569,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (n_src > 0) {
             uint32_t d = NEVER;
             if (has_stage) {
-                auto after = [&](int q) -> uint32_t {   // first step at which stage i's head is position q
-                    if (q == 0) return 0u;
-                    uint32_t c = p.cstep[i * L + q - 1];
-                    return c == NEVER ? NEVER : c + 1u;
-                };
+                // the base's last compute event before which stage i's head is still position q
+                auto after = [&](int q) -> uint32_t { return q == 0 ? 0u : p.cstep[i * L + q - 1]; };
                 int nbase = 0;
                 if (MOVES) {
                     if (mv.stage == i) {
@@ -649,8 +655,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     }
                 }
             }
-            ecount = ck_idx * p.ck_interval;
+            ecount = (int)src[ck_r + lane * CK_REGW + 20];
             ecount0 = ecount;
+            cc = ck_idx * p.ck_interval;
         } else {
             ecount0 = 0;
             pos = 0; sfree = 0; cfree = 0;
@@ -658,7 +665,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             n_poff = n_prel = 0;
             n_unrel = cand_unrel;
             first_start = INT_MAX; ecount = 0;
+            cc = 0;
         }
+        const int cc0 = cc;
         ovf = false;
         rF = rG = NO_R;
         head = fetch(pos); nxt = fetch(pos + 1);
@@ -670,44 +679,10 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         // ================= simulate: one committed event per iteration ===================
         bool ck_full = false;
         // a resumed recording starts from the previous base's widest window up to its checkpoint
-        int max_win = REC && ecount0 > 0 ? (int)p.ck[(size_t)(ecount0 / p.ck_interval) * p.ck_words + ck_r + 9] : 0;
+        int max_win = REC && cc0 > 0 ? (int)p.ck[(size_t)(cc0 / p.ck_interval) * p.ck_words + ck_r + 9] : 0;
         int conv_c = -1;
         for (;;) {
-            if (!REC && n_ck > 1) {
-                const int eb = ecount + eoff;
-                if (eb > 0 && ecount > (int)div && (eb & (p.ck_interval - 1)) == 0 && eb / p.ck_interval < n_ck) {
-                    const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead()));
-                    if (__all_sync(0xffffffffu, gate) && same_state(eb / p.ck_interval)) {
-                        conv_c = eb / p.ck_interval;
-                        break;
-                    }
-                }
-            }
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
-            // (a re-recording keeps the previous base's checkpoint it resumed from: same state)
-            if (REC && (ecount & (p.ck_interval - 1)) == 0 && !(ecount == ecount0 && ecount0 > 0)) {
-                const int c = ecount / p.ck_interval;
-                if (c < p.ck_max) {
-                    uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                    for (int q = lane; q < nz; q += 32) dst[q] = SW(o_A + (q));
-                    if (has_stage) {
-                        uint32_t *st = dst + ck_t + i * p.ck_kc;
-                        V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
-                        for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
-                    }
-                    const int ws0 = ws, we0 = we;
-                    we -= ws;
-                    ws = 0;
-                    save_regs(dst + ck_r + lane * CK_REGW);
-                    *reinterpret_cast<long long *>(dst + ck_r + lane * CK_REGW + 10) = (long long)segpk;
-                    dst[ck_r + lane * CK_REGW + 9] = (uint32_t)max_win;     // widest window so far
-                    segpk = 0;
-                    ws = ws0;
-                    we = we0;
-                } else {
-                    ck_full = true;
-                }
-            }
             if (cdirty) { compute_key(); cdirty = false; }
             if (tdirty) { transfer_key(); tdirty = false; }
             const unsigned long long key = min(ckey, tkey);
@@ -718,6 +693,45 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
 
             const int t = (int)mh;
             const int rank = (int)(ml >> 30);
+            if (rank == RANK_COMPUTE && (cc & (p.ck_interval - 1)) == 0) {
+                const int c = cc / p.ck_interval;
+                // Suffix sharing.  A re-recording converges onto the previous base the same way:
+                // it saves this checkpoint, then stops, and the remaining ones are the previous
+                // base's shifted (rec_shift_kernel).
+                if ((REC ? n_src > 1 : n_ck > 1) && cc > (int)div && c < n_src) {
+                    const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead()));
+                    if (__all_sync(0xffffffffu, gate) && same_state(c)) {
+                        conv_c = c;
+                        if (!REC) break;
+                    }
+                }
+                // (a re-recording keeps the previous base's checkpoint it resumed from: same state)
+                if (REC && !(cc == cc0 && cc0 > 0)) {
+                    if (c < p.ck_max) {
+                        uint32_t *dst = p.ck + (size_t)c * p.ck_words;
+                        for (int q = lane; q < nz; q += 32) dst[q] = SW(o_A + (q));
+                        if (has_stage) {
+                            uint32_t *st = dst + ck_t + i * p.ck_kc;
+                            V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
+                            for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
+                        }
+                        const int ws0 = ws, we0 = we;
+                        we -= ws;
+                        ws = 0;
+                        uint32_t *rg = dst + ck_r + lane * CK_REGW;
+                        save_regs(rg);
+                        *reinterpret_cast<long long *>(rg + 10) = (long long)segpk;
+                        rg[9] = (uint32_t)max_win;     // widest window so far
+                        rg[20] = (uint32_t)ecount;
+                        segpk = 0;
+                        ws = ws0;
+                        we = we0;
+                    } else {
+                        ck_full = true;
+                    }
+                }
+                if (REC && conv_c >= 0) break;
+            }
             const int w = (int)((ml >> 24) & 63u);
             const int j = (int)((ml >> 2) & 0x3FFFFFu);
             const int k = (int)(ml & 3u);
@@ -726,10 +740,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 p.tstart[(size_t)cand * p.tstride + ecount] = t;
             }
             if (REC && rank == RANK_COMPUTE && i == w) {
-                p.cstep[i * L + pos] = (uint32_t)ecount;
-                if (k == KIND_F) p.fstep[i * m + j] = (uint32_t)ecount;
+                p.cstep[i * L + pos] = (uint32_t)cc;
+                if (k == KIND_F) p.fstep[i * m + j] = (uint32_t)cc;
             }
             ++ecount;
+            if (rank == RANK_COMPUTE) ++cc;
             if (rank == RANK_COMPUTE) {
                 if (i == w) {
                     const int end = t + proc_of(j, k);
@@ -740,13 +755,27 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     head = nxt;
                     nxt = fetch(pos + 1);
                     if (first_start == INT_MAX) first_start = t;
+                    // End-time words keep their time only while a reader on another resource is to
+                    // come; readers on the op's own stage are bounded by its free time, so there the
+                    // time is dropped (canonical words).
                     if (k == KIND_F) {
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
                         if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
+                        if (i > 0) {
+                            // F(i, j) read A[i-1][j]; unless F(i-1, j)'s offload is still to come,
+                            // only B(i-1, j) reads it now
+                            const bool off_pending = ((SW(o_A + (2 * P * m + (i - 1) * MW + (j >> 5))) >> (j & 31)) & 1u) &&
+                                                     (SW(o_A + (P * m + (i - 1) * m + j)) & 3u) == 0u;
+                            if (!off_pending) SW(o_A + ((i - 1) * m + j)) = 1u;
+                        }
                     } else if (k == KIND_B) {
-                        SW(o_Ai + (j)) = ((uint32_t)end << 2) | 2u;
+                        SW(o_Ai + (j)) = i == 0 ? 2u : (((uint32_t)end << 2) | 2u);   // B(i-1, j) reads it
                         SW(o_Xi + (j)) = 0u;                        // B(i, j) was its last reader
-                        if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 3u) SW(o_A + ((i + 1) * m + j)) = A_DEAD;
+                        if (i + 1 < P) {
+                            // B(i, j) read A[i+1][j]: W(i+1, j) remains (state 2) or nobody (state 3)
+                            const uint32_t nb = SW(o_A + ((i + 1) * m + j));
+                            SW(o_A + ((i + 1) * m + j)) = (nb & 3u) == 3u ? A_DEAD : 2u;
+                        }
                     } else {
                         // W(i, j) is the last reader of A[i][j] unless B(i-1, j) is still to come
                         const bool up_done = i == 0 || (SW(o_A + ((i - 1) * m + j)) & 3u) >= 2u;
@@ -768,7 +797,10 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     const V g = val_of(j, 3);
                     const uint32_t bit = 1u << (j & 31);
                     if (rank == RANK_OFFLOAD) {
-                        SW(o_Xi + (j)) = ((uint32_t)end << 2) | 1u;
+                        // the reload's floor (this end) is bounded by the channel's free time: drop it;
+                        // F(i, j)'s end keeps a reader only if F(i+1, j) is still to come
+                        SW(o_Xi + (j)) = 1u;
+                        if (i == P - 1 || (SW(o_A + ((i + 1) * m + j)) & 3u) != 0u) SW(o_Ai + (j)) = 1u;
                         win_insert(end, -g);
                         if (derived) { SW(o_poff + (j >> 5)) &= ~bit; SW(o_prel + (j >> 5)) |= bit; --n_poff; ++n_prel; }
                     } else {
@@ -794,6 +826,50 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
 
         // ================= finished or deadlocked =========================================
+        if (REC && conv_c >= 0) {
+            // The new base continues as the previous one, conv_delta later: its outcome is the
+            // previous base's shifted, with this recording's peak prefix and early first starts.
+            const int dl = conv_delta;
+            const uint32_t fl = (uint32_t)p.base_info[1];
+            const uint32_t *rgc = p.ck + (size_t)conv_c * p.ck_words + ck_r + lane * CK_REGW;
+            const V sfx = (V)*reinterpret_cast<const long long *>(rgc + 18);   // previous base's S_c
+            const int hi = has_stage ? (int)p.base_res[2 + P + i] + dl : 0;
+            const int fs = !has_stage ? INT_MAX
+                         : first_start != INT_MAX ? first_start : (int)p.base_res[2 + 2 * P + i] + dl;
+            long long span = -1;
+            if (fl == FLAG_FEASIBLE) {
+                if (p.post) span = __reduce_max_sync(0xffffffffu, has_stage ? hi - fs : 0);
+                else span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, fs);
+            }
+            if (has_stage) {
+                p.base_res[2 + i] = fl == FLAG_FEASIBLE ? (long long)(peak > sfx ? peak : sfx) * p.unit : -1;
+                p.base_res[2 + P + i] = hi;
+                p.base_res[2 + 2 * P + i] = fs;
+                // suffix peaks of the checkpoints up to conv_c (later ones are unchanged)
+                long long run = (long long)sfx;
+                for (int c = conv_c; c >= 0; --c) {
+                    uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
+                    const long long sg = *reinterpret_cast<const long long *>(rg + 10);
+                    *reinterpret_cast<long long *>(rg + 18) = run;
+                    run = sg > run ? sg : run;
+                }
+            }
+            const int old_win = p.base_info[4], old_events = p.base_info[2];
+            __syncwarp();
+            if (lane == 0) {
+                p.base_info[2] = old_events - eoff;    // its transfer events differ by eoff
+                p.base_info[4] = max(max_win, old_win);
+                p.base_info[5] = conv_c;
+                p.base_info[6] = dl;
+                p.base_info[7] = eoff;
+                p.base_res[0] = span;
+                double b = span > 0 ? 1.0 - (double)p.busy / ((double)P * (double)span)
+                                    : __longlong_as_double(0x7ff8000000000000LL);
+                p.base_res[1] = __double_as_longlong(b);
+            }
+            __syncwarp();
+            continue;
+        }
         if (conv_c >= 0) {
             // converged onto the base: its outcome, with this candidate's peak prefix
             const uint32_t fl = (uint32_t)p.base_info[1];
@@ -846,7 +922,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             if (!unusable && has_stage) {
                 // S_c = max usage folded after checkpoint c (a converging candidate's peak suffix)
                 long long run = (long long)segpk;
-                for (int c = ecount / p.ck_interval; c >= 0; --c) {
+                for (int c = cc > 0 ? (cc - 1) / p.ck_interval : -1; c >= 0; --c) {
                     uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
                     const long long sg = *reinterpret_cast<const long long *>(rg + 10);
                     *reinterpret_cast<long long *>(rg + 18) = run;
@@ -854,7 +930,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 }
             }
             if (lane == 0) {
-                p.base_info[0] = unusable ? -1 : ecount / p.ck_interval + 1;
+                p.base_info[5] = -1;                      // no shifted suffix to apply
+                p.base_info[0] = unusable || cc == 0 ? -1 : (cc - 1) / p.ck_interval + 1;
                 p.base_info[4] = max_win;
                 p.base_info[1] = (int)(rem == 0u ? FLAG_FEASIBLE : FLAG_DEADLOCK);
                 p.base_info[2] = ecount;

@@ -188,6 +188,56 @@ def test_rerecorded_base_is_exact(cuda_ok, cfg):
         _eval_both(ls.di, o, mk, rb)
 
 
+def _base_tables(base, P, m, MW):
+    """A recorded base's tables with only what readers use: checkpoints up to the count, each
+    with its state words, the live window slots and every lane's saved scalars (all but word 9,
+    the widest window so far, a sizing hint)."""
+    from paper_2510_05186_b200 import _native as N
+    info = np.frombuffer(base.read(N.BASE_INFO), np.int32).copy()
+    res = np.frombuffer(base.read(N.BASE_RESULT), np.int64).copy()
+    cstep = np.frombuffer(base.read(N.BASE_CSTEP), np.uint32).copy()
+    fstep = np.frombuffer(base.read(N.BASE_FSTEP), np.uint32).copy()
+    raw = np.frombuffer(base.read(N.BASE_CHECKPOINTS), np.uint32)
+    ckw, ck_max, _, kc, ck_t, ck_u, ck_r, regw = np.frombuffer(base.read(N.BASE_LAYOUT), np.int32).tolist()
+    nz = 2 * P * m + 3 * P * MW
+    cks = []
+    for c in range(max(info[0], 0)):
+        w = raw[c * ckw:(c + 1) * ckw]
+        regs = w[ck_r:ck_r + regw * P].reshape(P, regw)
+        win = [(w[ck_t + s * kc: ck_t + s * kc + regs[s, 4]].tolist(),
+                w[ck_u + s * kc: ck_u + s * kc + regs[s, 4]].tolist()) for s in range(P)]
+        cks.append((w[:nz].tolist(), regs[:, list(range(9)) + list(range(10, 21))].tolist(), win))
+    return info[[0, 1, 2, 3]].tolist(), res.tolist(), cstep.tolist(), fstep.tolist(), cks
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_rerecording_equals_fresh_recording(cuda_ok, cfg):
+    """A base re-recorded over its predecessor — resumed from the predecessor's checkpoints and,
+    where it converges onto it, finished by shifting the predecessor's later checkpoints — leaves
+    exactly the tables a fresh recording does."""
+    import torch
+    from paper_2510_05186_b200.engine import Base
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    n = 512
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT, share_prefix=True))
+    pk = ls.di.packed
+    P, m, MW = pk.num_stages, pk.num_microbatches, (pk.num_microbatches + 31) // 32
+    o, mk = ls.materialize(0, n, 2)
+    r = ls.di.evaluate(o, mk, peak=False)
+    torch.cuda.synchronize()
+    flags, spans = r.flags.cpu().numpy(), r.makespan.cpu().numpy()
+    feas = np.nonzero(flags & 1)[0]
+    order = feas[np.argsort(spans[feas], kind="stable")]
+    picks = [int(x) for x in list(order[:4]) + list(order[-2:])] + [int(np.nonzero(flags & 2)[0][0])]
+    for idx in picks:
+        fresh, again = Base(ls.di), Base(ls.di)
+        fresh.record(o[idx], mk[idx])
+        again.record(ls.inc_orders, ls.inc_mask)
+        again.record(o[idx], mk[idx])
+        assert _base_tables(fresh, P, m, MW) == _base_tables(again, P, m, MW), idx
+
+
 def test_host_buffer_path_matches_device_path(cuda_ok):
     """ps_eval_batch_host (chunked, copies overlapped) == ps_eval_batch on the same candidates."""
     import torch
