@@ -92,13 +92,15 @@ typedef struct ps_instance_info {
 /* A batch of candidate structures, device memory. */
 typedef struct ps_cand_batch {
     int64_t num_candidates;
-    const uint16_t *stage_orders;   /* [N][P][order_stride] op codes, each row a permutation of the
-                                       stage's 3m ops                                               */
+    const void *stage_orders;       /* [N][P][order_stride] op codes, each row a permutation of the
+                                       stage's 3m ops; uint16 codes, or uint8 (order_bytes = 1)    */
     const uint32_t *offload_mask;   /* [N][mask_words]                                               */
     const uint32_t *channel_orders; /* [N][G][chan_stride] or NULL = derived (greedy) channel mode   */
     int32_t chan_stride;
     const ps_base *base;            /* optional recorded base (derived mode, no trace): shared
                                        prefixes are restored instead of re-simulated            */
+    int32_t order_bytes;            /* 2 (or 0): uint16 op codes; 1: uint8 op codes (m <= 64), half
+                                       the bytes to move — what ps_eval_batch_host copies in    */
 } ps_cand_batch;
 
 /* Per-candidate outputs, device memory.  Optional arrays may be NULL. */

@@ -75,6 +75,7 @@ class CandBatch(C.Structure):
         ("channel_orders", C.c_void_p),
         ("chan_stride", C.c_int32),
         ("base", C.c_void_p),
+        ("order_bytes", C.c_int32),
     ]
 
 

@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -108,9 +109,12 @@ struct Plan {
     size_t scratch_bytes;
 };
 
-int words_per_candidate(const ps_instance *I, int K) {
+// Per-candidate state words: ledger windows, end-time rows and bitsets, then (materialised
+// candidates, order_bytes > 0) the staged stage orders.
+int words_per_candidate(const ps_instance *I, int K, int order_bytes = 0) {
     int vw = I->v64 ? 2 : 1;
-    int w = I->P * 2 * K * (vw + 1) + 2 * I->P * I->m + 3 * I->P * I->MW;
+    int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
+    int w = I->P * 2 * K * (vw + 1) + ((nz + 1) & ~1) + I->P * I->stride * order_bytes / 4;
     return (w + 3) & ~3;
 }
 
@@ -149,9 +153,9 @@ int window_size(const ps_instance *I) { return std::min(std::max(4, env_int("PS_
 // One evaluation pass with ledger window K: one candidate per warp, as many warps per block as fit
 // in shared memory; the state moves to global memory only when a single warp's does not fit.
 // `N` bounds the grid (a worklist pass may receive fewer candidates, never more).
-int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl) {
+int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int order_bytes = 2) {
     pl->K = K;
-    pl->cand_words = words_per_candidate(I, K);
+    pl->cand_words = words_per_candidate(I, K, moves ? 0 : order_bytes);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
     pl->warps = 4;
@@ -238,7 +242,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
     const bool dynamic = env_int("PS_DYNAMIC", 1) != 0;
     for (int k = 0; k < npass; ++k) {
         Plan pl;
-        int rc = plan_pass(I, moves, Ks[k], p.N, &pl);
+        int rc = plan_pass(I, moves, Ks[k], p.N, &pl, p.order_u8 ? 1 : 2);
         if (rc) return rc;
         EvalParams q = p;
         q.K = pl.K;
@@ -251,6 +255,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.ovf_count = out;
         q.ovf_list = out ? out + 1 : nullptr;
         q.work_next = dynamic ? lists + 2 * list_words + k : nullptr;
+        if (k > 0) q.ready = nullptr;       // later passes start after the first has read everything
         uint32_t *scratch = nullptr;
         if (pl.scratch_bytes) PS_CUDA(cudaMallocAsync((void **)&scratch, pl.scratch_bytes, s));
         q.gstate = scratch;
@@ -564,7 +569,7 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     B->inst = I;
     B->K = std::min(5 * I->m, 128);                 // recording window (checkpoints store it compactly)
     B->max_window = -1;
-    B->cand_words = words_per_candidate(I, B->K);
+    B->cand_words = words_per_candidate(I, B->K, 2);
     {
         const int vw = I->v64 ? 2 : 1;
         const int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
@@ -709,13 +714,25 @@ int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
     return PS_OK;
 }
 
+static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r,
+                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk);
+
 int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
+    return eval_batch_impl(I, b, r, (cudaStream_t)stream, nullptr, 0);
+}
+
+static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r,
+                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk) {
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
     if (b->num_candidates < 0) return fail(PS_ERR_INVALID, "negative candidate count");
     if (b->num_candidates == 0) return PS_OK;
     if (!b->stage_orders || !b->offload_mask) return fail(PS_ERR_INVALID, "stage_orders and offload_mask are required");
     if (!r->makespan || !r->flags || !r->bubble) return fail(PS_ERR_INVALID, "makespan, bubble and flags outputs are required");
     if (b->channel_orders && b->chan_stride < 1) return fail(PS_ERR_INVALID, "chan_stride must be positive");
+    if (b->order_bytes != 0 && b->order_bytes != 1 && b->order_bytes != 2)
+        return fail(PS_ERR_INVALID, "order_bytes must be 1 or 2");
+    if (b->order_bytes == 1 && 4 * I->m > 256) return fail(PS_ERR_RANGE, "uint8 op codes need m <= 64");
+    if ((uintptr_t)b->stage_orders & 7u) return fail(PS_ERR_INVALID, "stage_orders must be 8-byte aligned");
     if ((r->trace_code != nullptr) != (r->trace_start != nullptr))
         return fail(PS_ERR_INVALID, "trace_code and trace_start go together");
     if (r->trace_code && r->trace_stride < 5 * I->P * I->m)
@@ -727,6 +744,7 @@ int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_
     fill_instance(I, &p);
     p.N = b->num_candidates;
     p.orders = b->stage_orders;
+    p.order_u8 = b->order_bytes == 1;
     p.masks = b->offload_mask;
     p.chorders = b->channel_orders;
     p.chan_stride = b->chan_stride;
@@ -739,40 +757,65 @@ int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_
     p.tstart = r->trace_start;
     p.tstride = r->trace_stride;
     p.events_total = (unsigned long long *)r->events_total;
-    return run_eval(I, p, false, (cudaStream_t)stream, b->base);
+    p.ready = ready;
+    p.ready_chunk = ready_chunk;
+    return run_eval(I, p, false, stream, b->base);
+}
+
+// Pinned host word holding 1: the copy engine writes it behind each chunk as its ready flag.
+static const int32_t *pinned_one() {
+    static int32_t *one = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (cudaHostAlloc((void **)&one, sizeof(int32_t), cudaHostAllocPortable) == cudaSuccess) *one = 1;
+        else one = nullptr;
+    });
+    return one;
 }
 
 int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
     const int64_t N = b->num_candidates;
     if (N <= 0) return N == 0 ? PS_OK : fail(PS_ERR_INVALID, "negative candidate count");
+    if (!b->stage_orders || !b->offload_mask) return fail(PS_ERR_INVALID, "stage_orders and offload_mask are required");
+    if (r->events_total) return fail(PS_ERR_INVALID, "events_total is a device counter: use ps_eval_batch");
+    if (b->order_bytes != 0 && b->order_bytes != 1 && b->order_bytes != 2)
+        return fail(PS_ERR_INVALID, "order_bytes must be 1 or 2");
+    const int ob = b->order_bytes == 1 ? 1 : 2;
+    if (ob == 1 && 4 * I->m > 256) return fail(PS_ERR_RANGE, "uint8 op codes need m <= 64");
     DeviceGuard guard(I->device);
     if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    const int32_t *one = pinned_one();
+    if (!one) return fail(PS_ERR_NOMEM, "pinned flag word");
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t n_ord = (size_t)N * I->P * I->stride * 2, n_mask = (size_t)N * I->mask_words * 4;
+    // Inputs stream in over PCIe in chunks on a copy stream while ONE evaluation launch runs: the
+    // copy engine writes a ready flag behind each chunk and warps wait for their candidate's flag
+    // (candidates are taken in index order), so copy and evaluation overlap without wave tails.
+    const int64_t chunk = std::max<int64_t>(1, env_int("PS_HOST_CHUNK", 4096));
+    const int nchunks = (int)((N + chunk - 1) / chunk);
+    const size_t n_ord = (size_t)N * I->P * I->stride * ob, n_mask = (size_t)N * I->mask_words * 4;
     const size_t n_chan = b->channel_orders ? (size_t)N * I->G * b->chan_stride * 4 : 0;
     const size_t n_peak = r->peak ? (size_t)N * I->P * 8 : 0;
     const size_t n_tr = r->trace_code ? (size_t)N * r->trace_stride * 4 : 0;
     const size_t n_blk = r->blocked ? (size_t)N * 4 : 0;
-    if (r->events_total) return fail(PS_ERR_INVALID, "events_total is a device counter: use ps_eval_batch");
-    // one device arena: inputs, then outputs
-    size_t off[10], total = 0;
-    size_t sizes[10] = {n_ord, n_mask, n_chan, (size_t)N * 8, (size_t)N * 8, n_peak, (size_t)N * 4, n_blk, n_tr, n_tr};
-    for (int k = 0; k < 10; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
+    // one device arena: inputs, ready flags, outputs
+    size_t off[11], total = 0;
+    size_t sizes[11] = {n_ord, n_mask, n_chan, (size_t)nchunks * 4, (size_t)N * 8, (size_t)N * 8, n_peak,
+                        (size_t)N * 4, n_blk, n_tr, n_tr};
+    for (int k = 0; k < 11; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
     char *arena = nullptr;
     PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
-    // Inputs cross PCIe on a copy stream, in chunks the evaluation waits for one at a time.  One
-    // chunk by default: measured on B200 (r01), splitting a 65,536-candidate batch into 4 launches
-    // costs more in wave tails than the ~4 ms of copy it hides.
-    const int64_t chunk = std::max<int64_t>(1, env_int("PS_HOST_CHUNK", (int)std::min<int64_t>(N, INT32_MAX)));
-    const int nchunks = (int)((N + chunk - 1) / chunk);
+    int32_t *ready = (int32_t *)(arena + off[3]);
+    PS_CUDA(cudaMemsetAsync(ready, 0, (size_t)nchunks * 4, s));
     cudaStream_t cs = nullptr;
-    std::vector<cudaEvent_t> ev(nchunks + 1, nullptr);
+    cudaEvent_t ev_start = nullptr, ev_copied = nullptr;
     PS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    for (auto &e : ev) PS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    PS_CUDA(cudaEventRecord(ev[nchunks], s));                    // the arena exists on s
-    PS_CUDA(cudaStreamWaitEvent(cs, ev[nchunks], 0));
-    const size_t ord_row = (size_t)I->P * I->stride * 2, mask_row = (size_t)I->mask_words * 4;
+    PS_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    PS_CUDA(cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming));
+    PS_CUDA(cudaEventRecord(ev_start, s));                  // arena and cleared flags exist
+    PS_CUDA(cudaStreamWaitEvent(cs, ev_start, 0));
+    // every copy is enqueued before the evaluation launches: the flags it waits for are certain
+    const size_t ord_row = (size_t)I->P * I->stride * ob, mask_row = (size_t)I->mask_words * 4;
     const size_t chan_row = b->channel_orders ? (size_t)I->G * b->chan_stride * 4 : 0;
     for (int c = 0; c < nchunks; ++c) {
         const int64_t lo = c * chunk, n = std::min(chunk, N - lo);
@@ -783,43 +826,39 @@ int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_re
         if (n_chan)
             PS_CUDA(cudaMemcpyAsync(arena + off[2] + lo * chan_row, (const char *)b->channel_orders + lo * chan_row,
                                     n * chan_row, cudaMemcpyHostToDevice, cs));
-        PS_CUDA(cudaEventRecord(ev[c], cs));
+        PS_CUDA(cudaMemcpyAsync(ready + c, one, sizeof(int32_t), cudaMemcpyHostToDevice, cs));
     }
-    int rc = PS_OK;
-    for (int c = 0; c < nchunks && rc == PS_OK; ++c) {
-        const int64_t lo = c * chunk, n = std::min(chunk, N - lo);
-        PS_CUDA(cudaStreamWaitEvent(s, ev[c], 0));
-        ps_cand_batch db = *b;
-        db.num_candidates = n;
-        db.stage_orders = (const uint16_t *)(arena + off[0] + lo * ord_row);
-        db.offload_mask = (const uint32_t *)(arena + off[1] + lo * mask_row);
-        db.channel_orders = n_chan ? (const uint32_t *)(arena + off[2] + lo * chan_row) : nullptr;
-        ps_result_batch dr = *r;
-        dr.makespan = (int64_t *)(arena + off[3]) + lo;
-        dr.bubble = (double *)(arena + off[4]) + lo;
-        dr.peak = n_peak ? (int64_t *)(arena + off[5]) + lo * I->P : nullptr;
-        dr.flags = (uint32_t *)(arena + off[6]) + lo;
-        dr.blocked = n_blk ? (uint32_t *)(arena + off[7]) + lo : nullptr;
-        dr.trace_code = n_tr ? (uint32_t *)(arena + off[8]) + lo * r->trace_stride : nullptr;
-        dr.trace_start = n_tr ? (int32_t *)(arena + off[9]) + lo * r->trace_stride : nullptr;
-        rc = ps_eval_batch(I, &db, &dr, stream);
-        if (rc) break;
-        PS_CUDA(cudaMemcpyAsync(r->makespan + lo, dr.makespan, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-        PS_CUDA(cudaMemcpyAsync(r->bubble + lo, dr.bubble, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-        PS_CUDA(cudaMemcpyAsync(r->flags + lo, dr.flags, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
-        if (n_peak) PS_CUDA(cudaMemcpyAsync(r->peak + lo * I->P, dr.peak, (size_t)n * I->P * 8, cudaMemcpyDeviceToHost, s));
-        if (n_blk) PS_CUDA(cudaMemcpyAsync(r->blocked + lo, dr.blocked, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaEventRecord(ev_copied, cs));
+    ps_cand_batch db = *b;
+    db.stage_orders = arena + off[0];
+    db.offload_mask = (const uint32_t *)(arena + off[1]);
+    db.channel_orders = n_chan ? (const uint32_t *)(arena + off[2]) : nullptr;
+    ps_result_batch dr = *r;
+    dr.makespan = (int64_t *)(arena + off[4]);
+    dr.bubble = (double *)(arena + off[5]);
+    dr.peak = n_peak ? (int64_t *)(arena + off[6]) : nullptr;
+    dr.flags = (uint32_t *)(arena + off[7]);
+    dr.blocked = n_blk ? (uint32_t *)(arena + off[8]) : nullptr;
+    dr.trace_code = n_tr ? (uint32_t *)(arena + off[9]) : nullptr;
+    dr.trace_start = n_tr ? (int32_t *)(arena + off[10]) : nullptr;
+    int rc = eval_batch_impl(I, &db, &dr, s, ready, chunk);
+    cudaStreamWaitEvent(s, ev_copied, 0);
+    if (rc == PS_OK) {
+        PS_CUDA(cudaMemcpyAsync(r->makespan, dr.makespan, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(r->bubble, dr.bubble, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(r->flags, dr.flags, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
+        if (n_peak) PS_CUDA(cudaMemcpyAsync(r->peak, dr.peak, n_peak, cudaMemcpyDeviceToHost, s));
+        if (n_blk) PS_CUDA(cudaMemcpyAsync(r->blocked, dr.blocked, n_blk, cudaMemcpyDeviceToHost, s));
         if (n_tr) {
-            const size_t tb = (size_t)n * r->trace_stride * 4;
-            PS_CUDA(cudaMemcpyAsync(r->trace_code + lo * r->trace_stride, dr.trace_code, tb, cudaMemcpyDeviceToHost, s));
-            PS_CUDA(cudaMemcpyAsync(r->trace_start + lo * r->trace_stride, dr.trace_start, tb, cudaMemcpyDeviceToHost, s));
+            PS_CUDA(cudaMemcpyAsync(r->trace_code, dr.trace_code, n_tr, cudaMemcpyDeviceToHost, s));
+            PS_CUDA(cudaMemcpyAsync(r->trace_start, dr.trace_start, n_tr, cudaMemcpyDeviceToHost, s));
         }
     }
-    // every copy of cs precedes an event s waited on, so s alone now orders the free and the sync
-    cudaStreamSynchronize(cs);
     cudaFreeAsync(arena, s);
     cudaError_t e = cudaStreamSynchronize(s);
-    for (auto &x : ev) cudaEventDestroy(x);
+    cudaStreamSynchronize(cs);
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_copied);
     cudaStreamDestroy(cs);
     if (rc) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "ps_eval_batch_host");

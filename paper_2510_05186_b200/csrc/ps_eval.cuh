@@ -46,7 +46,8 @@ struct EvalParams {
     const int32_t *chan;     // [P]
     // materialised candidates
     int64_t N;
-    const uint16_t *orders;
+    const void *orders;      // uint16 op codes, or uint8 when order_u8
+    int order_u8;
     const uint32_t *masks;
     const uint32_t *chorders;
     int chan_stride;
@@ -71,6 +72,10 @@ struct EvalParams {
     int32_t *ovf_list;
     int32_t *ovf_count;
     int32_t *work_next;      // dynamic candidate distribution (NULL: static grid stride)
+    // streamed inputs (host-buffer evaluation): candidate c may be read once ready[c / ready_chunk]
+    // is non-zero; the copy engine writes each flag after its chunk's data, on the same stream
+    const int32_t *ready;
+    long long ready_chunk;
     const int32_t *work_list;
     const int32_t *work_count;
     // per-candidate state
@@ -111,10 +116,11 @@ __device__ __forceinline__ unsigned long long make_key(uint32_t hi, uint32_t lo)
 }
 constexpr unsigned long long KEY_ABSENT = ~0ull;
 
-// 64 registers per thread (8 blocks of 4 warps per SM) measured best on B200 for the
-// shared-memory variants (tools/kexp.py); the global-state variant keeps its registers.
+// 72 registers per thread (7 blocks of 4 warps per SM) measured best on B200 for the
+// shared-memory variants (tools/kvar.py: 64 spills the event loop's keys, 80+ loses warps);
+// the global-state variant keeps its registers.
 #ifndef PS_MIN_BLOCKS
-#define PS_MIN_BLOCKS 8
+#define PS_MIN_BLOCKS 7
 #endif
 #ifndef PS_TAU_PAIR
 #define PS_TAU_PAIR 0   // measured slower on B200 (r01): register pressure outweighs the saved scan
@@ -163,6 +169,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     const int o_poff = o_offm + P * MW;                         // [P][MW] pending offload requests
     const int o_prel = o_poff + P * MW;                         // [P][MW] pending reload requests
     const int nz = 2 * P * m + 3 * P * MW;               // words zeroed per candidate
+    // materialised candidates: the candidate's stage orders, staged once (8-byte aligned)
+    const int o_row = o_A + ((nz + 1) & ~1);
+    const int row_bytes = P * p.stride * (p.order_u8 ? 1 : 2);
 
     const int chan_i = has_stage ? __ldg(&p.chan[i]) : -1;
     const V limit_i = has_stage ? ldv<V>(p.limit, i) : V(0);
@@ -213,13 +222,28 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     int lastq = -1;     // last position of this stage's order that differs from the base's
     int eoff = 0;       // base step = candidate step + eoff once the candidate's extra/missing transfers are done
 
+    // op code idx of the staged candidate rows ([P][stride], uint8 or uint16)
+    auto row_at = [&](int idx) -> uint32_t {
+        const unsigned char *rb = GSTATE ? reinterpret_cast<const unsigned char *>(gsw + o_row)
+                                         : reinterpret_cast<const unsigned char *>(smem + sbase + o_row);
+        return p.order_u8 ? (uint32_t)rb[idx] : (uint32_t)reinterpret_cast<const uint16_t *>(rb)[idx];
+    };
+    // eight op codes from position q (a multiple of 8) of stage i's staged row, as uint16 pairs
+    auto row8 = [&](int q) -> uint4 {
+        const unsigned char *rb = GSTATE ? reinterpret_cast<const unsigned char *>(gsw + o_row)
+                                         : reinterpret_cast<const unsigned char *>(smem + sbase + o_row);
+        if (!p.order_u8) return *reinterpret_cast<const uint4 *>(rb + 2 * (i * p.stride + q));
+        const uint2 b = *reinterpret_cast<const uint2 *>(rb + i * p.stride + q);
+        return make_uint4(__byte_perm(b.x, 0u, 0x4140), __byte_perm(b.x, 0u, 0x4342),
+                          __byte_perm(b.y, 0u, 0x4140), __byte_perm(b.y, 0u, 0x4342));
+    };
     auto fetch = [&](int q) -> uint32_t {
         if (q >= L || !has_stage) return 0u;
         if (MOVES) {
             int src = (mv.type == MOVE_SHIFT && i == mv.stage) ? shifted_position(q, mv.a, mv.b) : q;
             return inc_s[i * p.stride + src];
         }
-        return __ldg(&p.orders[((size_t)cand * P + i) * p.stride + q]);
+        return row_at(i * p.stride + q);
     };
     auto fetch_chan = [&](int q) -> uint32_t {
         if (derived || !has_stage || q >= p.chan_stride) return NO_CHAN;
@@ -506,8 +530,28 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     };
     for (; item < n_items; item = next_item()) {
         cand = p.work_list ? (long long)p.work_list[item] : item;
+        if (p.ready) {
+            // this candidate's chunk may still be crossing PCIe: wait for its flag
+            if (lane == 0) {
+                const volatile int32_t *f = p.ready + cand / p.ready_chunk;
+                // (bounded: a flag that never comes — a failed copy — aborts the launch, ~10 s)
+                for (unsigned spins = 0; *f == 0; ++spins) {
+                    if (spins > (1u << 25)) __trap();
+                    __nanosleep(256);
+                }
+                __threadfence();
+            }
+            __syncwarp();
+        }
         // ================= initialise ======================================================
         for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = 0u;
+        if (!MOVES) {
+            // stage the candidate's rows: 8-byte loads, coalesced across the warp
+            const uint2 *src = reinterpret_cast<const uint2 *>(reinterpret_cast<const unsigned char *>(p.orders) +
+                                                               (size_t)cand * row_bytes);
+            uint2 *dst = GSTATE ? reinterpret_cast<uint2 *>(gsw + o_row) : reinterpret_cast<uint2 *>(smem + sbase + o_row);
+            for (int k = lane; k < row_bytes / 8; k += 32) dst[k] = __ldcg(src + k);   // (L2: may be streamed in)
+        }
         if (MOVES) {
             uint64_t gidx = (uint64_t)(p.first_index + cand);
             mv = decode_move(p.seed, p.round, gidx, P, m, p.shift_permille, p.max_shift, p.any_off != 0,
@@ -524,7 +568,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 const int gb = i * m + w * 32, q = gb >> 5, sh = gb & 31;
                 auto word = [&](int qq) -> uint32_t {
                     if (qq >= mwords) return 0u;
-                    return MOVES ? incmask_s[qq] : __ldg(&p.masks[(size_t)cand * mwords + qq]);
+                    return MOVES ? incmask_s[qq] : __ldcg(&p.masks[(size_t)cand * mwords + qq]);
                 };
                 uint32_t bits = word(q) >> sh;
                 if (sh) bits |= word(q + 1) << (32 - sh);
@@ -544,17 +588,27 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (has_stage) {
             cand_unrel = build_mask(true);
             if (!MOVES) {
-                // the stage order must be a permutation of the stage's 3m ops
-                for (int q = 0; q < L; ++q) {
-                    uint32_t op = __ldg(&p.orders[((size_t)cand * P + i) * p.stride + q]);
-                    uint32_t j = op >> 2, k = op & 3u;
-                    if (j >= (uint32_t)m || k > 2u || (SW(o_Ai + (j)) >> k) & 1u) { bad = true; break; }
-                    SW(o_Ai + (j)) |= 1u << k;
+                // the stage order must be a permutation of the stage's 3m ops: 3m valid codes
+                // without a repeat (seen-sets in registers up to m = 64, else in the A row)
+                if (m <= 64) {
+                    unsigned long long fm = 0ull, bm = 0ull, wm = 0ull;
+                    for (int q = 0; q < L; ++q) {
+                        const uint32_t op = row_at(i * p.stride + q), j = op >> 2, k = op & 3u;
+                        if (j >= (uint32_t)m || k > 2u) { bad = true; break; }
+                        const unsigned long long bit = 1ull << j;
+                        const unsigned long long seen = k == 0u ? fm : (k == 1u ? bm : wm);
+                        if (seen & bit) { bad = true; break; }
+                        if (k == 0u) fm |= bit; else if (k == 1u) bm |= bit; else wm |= bit;
+                    }
+                } else {
+                    for (int q = 0; q < L; ++q) {
+                        uint32_t op = row_at(i * p.stride + q);
+                        uint32_t j = op >> 2, k = op & 3u;
+                        if (j >= (uint32_t)m || k > 2u || (SW(o_Ai + (j)) >> k) & 1u) { bad = true; break; }
+                        SW(o_Ai + (j)) |= 1u << k;
+                    }
+                    for (int j = 0; j < m; ++j) SW(o_Ai + (j)) = 0u;
                 }
-                if (!bad)
-                    for (int j = 0; j < m; ++j)
-                        if (SW(o_Ai + (j)) != 7u) { bad = true; break; }
-                for (int j = 0; j < m; ++j) SW(o_Ai + (j)) = 0u;
             }
         }
         if (__any_sync(0xffffffffu, bad)) {
@@ -579,14 +633,25 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     }
                     for (int w = 0; w < MW; ++w) nbase += __popc(base_word(w));
                 } else {
-                    const uint16_t *row = p.orders + ((size_t)cand * P + i) * p.stride;
+                    // first and last position where the row differs from the base's, eight codes
+                    // at a time (rows are padded to a multiple of 8; the padding never differs
+                    // inside [0, L) bounds)
                     const uint16_t *brow = p.base_orders + (size_t)i * p.stride;
+                    auto differs8 = [&](int q) -> bool {
+                        const uint4 a = row8(q), b = __ldg(reinterpret_cast<const uint4 *>(brow + q));
+                        return a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
+                    };
                     int q = 0;
-                    while (q < L && row[q] == brow[q]) ++q;
+                    while (q + 8 <= L && !differs8(q)) q += 8;
+                    while (q < L && row_at(i * p.stride + q) == brow[q]) ++q;
                     if (q < L) {
                         d = after(q);
-                        lastq = L - 1;
-                        while (lastq > q && row[lastq] == brow[lastq]) --lastq;
+                        int e = L - 1;          // every position above e is equal
+                        while (e > q && ((e + 1) & 7) && row_at(i * p.stride + e) == brow[e]) --e;
+                        if (((e + 1) & 7) == 0)
+                            while (e - 7 > q && !differs8(e - 7)) e -= 8;
+                        while (e > q && row_at(i * p.stride + e) == brow[e]) --e;
+                        lastq = e;
                     }
                     for (int w = 0; w < MW; ++w) {
                         const uint32_t bb = base_word(w);
@@ -731,6 +796,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     }
                 }
                 if (REC && conv_c >= 0) break;
+                __syncwarp();      // the checkpoint's reads before the commit's writes
             }
             const int w = (int)((ml >> 24) & 63u);
             const int j = (int)((ml >> 2) & 0x3FFFFFu);
@@ -812,7 +878,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     // the ledger changed: an F head re-fits; a B head may have been waiting on this reload
                     cdirty = cdirty || (pos < L && ((head & 3u) == KIND_F || head == (((uint32_t)j << 2) | KIND_B)));
                 }
-                if (has_stage && chan_i == __ldg(&p.chan[w])) {
+                const int wchan = __shfl_sync(0xffffffffu, chan_i, w);   // (warp-uniform branch)
+                if (has_stage && chan_i == wchan) {
                     cfree = end;
                     tdirty = true;
                     if (!derived) {

@@ -95,9 +95,11 @@ class DeviceInstance:
             trace_start=torch.empty((n, E), dtype=torch.int32, device=dev) if trace else None)
 
     def _batch_structs(self, n, orders, masks, chans, res: EvalResult, base=None):
+        # uint8 op codes (m <= 64) halve what crosses PCIe; int16/uint16 are the general form
+        one_byte = str(orders.dtype) in ("uint8", "torch.uint8")
         cb = N.CandBatch(n, _ptr(orders), _ptr(masks), _ptr(chans),
                          int(chans.shape[-1]) if chans is not None else 0,
-                         base.handle if base is not None else None)
+                         base.handle if base is not None else None, 1 if one_byte else 2)
         rb = N.ResultBatch(_ptr(res.makespan), _ptr(res.bubble), _ptr(res.peak), _ptr(res.flags),
                            _ptr(res.blocked), _ptr(res.trace_code), _ptr(res.trace_start),
                            int(res.trace_code.shape[-1]) if res.trace_code is not None else 0)

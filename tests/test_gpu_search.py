@@ -249,8 +249,10 @@ def test_host_buffer_path_matches_device_path(cuda_ok):
     torch.cuda.synchronize()
     h_o = o.cpu().numpy()
     h_m = mk.cpu().numpy()
-    for base in (None, ls.base):
-        host = ls.di.evaluate_host(h_o, h_m, peak=True, base=base)
+    h_o8 = h_o.astype(np.uint8)                      # m = 64: op codes fit in one byte
+    assert (h_o8.astype(np.int16) == h_o).all()
+    for base, ho in ((None, h_o), (ls.base, h_o), (None, h_o8), (ls.base, h_o8)):
+        host = ls.di.evaluate_host(ho, h_m, peak=True, base=base)
         assert (host.flags == dev.flags.cpu().numpy()).all()
         assert (host.makespan == dev.makespan.cpu().numpy()).all()
         assert (host.peak == dev.peak.cpu().numpy()).all()

@@ -1,0 +1,44 @@
+"""Diagnostic: where the host-buffer evaluation's time goes (H2D alone, device eval alone, total)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2510_05186_b200 import workloads  # noqa: E402
+from paper_2510_05186_b200.heuristics import best_feasible  # noqa: E402
+from paper_2510_05186_b200.listsched import stage_order_of  # noqa: E402
+from paper_2510_05186_b200.search import LocalSearch, SearchConfig  # noqa: E402
+
+inst = workloads.CONFIGS[3]()
+s0, _ = best_feasible(inst)
+orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
+n = 65536
+ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=n, shift_permille=700, max_shift=4))
+od, md = ls.materialize(0, n)
+od8 = od.to(torch.uint8)
+h8 = torch.empty(od8.shape, dtype=torch.uint8, pin_memory=True)
+h8.copy_(od8)
+hm = torch.empty(md.shape, dtype=torch.int32, pin_memory=True)
+hm.copy_(md)
+dev8 = torch.empty_like(od8)
+
+
+def t(fn, reps=5):
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        fn()
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - a)
+    return 1000 * sorted(ts)[len(ts) // 2]
+
+
+print("h2d 8-bit orders  ms", t(lambda: dev8.copy_(h8, non_blocking=True)), "bytes", h8.numel())
+print("eval device u8    ms", t(lambda: ls.di.evaluate(od8, md, peak=True, base=ls.base)))
+print("eval device u16   ms", t(lambda: ls.di.evaluate(od, md, peak=True, base=ls.base)))
+print("eval device nobase ms", t(lambda: ls.di.evaluate(od8, md, peak=True)))
+ho, hmm = h8.numpy(), hm.numpy()
+print("eval host u8      ms", t(lambda: ls.di.evaluate_host(ho, hmm, peak=True, base=ls.base)))

@@ -1,1 +1,3 @@
-for iv in 4 8 16; do PS_CHECKPOINT_INTERVAL=$iv timeout 300 python bench.py --no-cpu --no-e2e --steps 6 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('interval', $iv, d['value'], d['ms_per_step'], d['roofline']['kernel_ms_per_launch'], d['roofline']['events_per_launch'], d['search']['final_makespan'])"; done
+timeout 300 python tools/prefix_diff.py 4 2>&1 | tail -1
+NCAND=256 REPS=1 timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool initcheck --print-limit 3 python tools/prefix_diff.py 2 > gpurun_out/initcheck.txt 2>&1; grep -A3 "Uninit" gpurun_out/initcheck.txt | head -12; grep "SUMMARY" gpurun_out/initcheck.txt
+timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
