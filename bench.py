@@ -52,7 +52,8 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled during the timed region: NVML every 5 ms (the timed
+    region is a fraction of a second), nvidia-smi every 200 ms when NVML is unavailable."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -63,8 +64,34 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self._nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(phys))
+        except Exception:
+            self._nvml = None
+
+    def _run_nvml(self):
+        nv, h = self._nvml
+        masks = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                 nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append([str(self.index), str(sm), str(mx)] +
+                                 ["Active" if r & mk else "Not Active" for mk in masks])
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def _run(self):
+        if self._nvml is not None:
+            return self._run_nvml()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
@@ -172,13 +199,15 @@ def workload_config(world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=3.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttb", action="store_true")
+    ap.add_argument("--ttb-rounds", type=int, default=1000)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -204,7 +233,7 @@ def main():
     cfg = SearchConfig(seed=SEED, neighbours=PER_GPU * world, **MOVES)
     ls = LocalSearch(inst, orders0, s0.offloaded, cfg, device=local)
     lib, di = ls.lib, ls.di
-    events_total = torch.zeros(1, dtype=torch.int64, device=dev)
+    events_total = torch.zeros(2, dtype=torch.int64, device=dev)   # [simulated, algorithmic] events
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def round_timed(ev_k0, ev_k1):
@@ -251,7 +280,9 @@ def main():
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_s = float(total_ms.item()) / 1e3
     value = cfg.neighbours * K / total_s
-    launches = 2 * K + improved        # evaluator main + overflow pass per round, apply_move per improvement
+    # per round: the evaluator's main pass and its two overflow passes; per improvement: apply_move,
+    # the base re-recording and its checkpoint shift
+    launches = 3 * K + 3 * improved
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": 1000 * total_s / K, "higher_is_better": True,
@@ -259,9 +290,10 @@ def main():
             "config": workload_config(world), "clocks": clk.summary(), "gpu_launches": launches}
 
     # ---- roofline: INT32 issue ----------------------------------------------------
-    ev_total = int(events_total.item())
+    ev_sim, ev_full = (int(x) for x in events_total.tolist())
     kern_s = sum(kern_ms) / 1e3 / K
-    ops_per_launch = 10 * ev_total / K
+    # W_c = 10 int ops per event of every evaluated candidate, E_c = 3Pm + 2|off_c|
+    ops_per_launch = 10 * ev_full / K
     probe = torch.zeros(1, dtype=torch.int64, device=dev)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     N.check(lib.ps_int32_probe(200, C.c_void_p(probe.data_ptr()), C.c_void_p(stream.cuda_stream)))
@@ -283,14 +315,17 @@ def main():
     line["roofline"] = {
         "bound": "int32-issue", "achieved": achieved, "peak": int32_peak, "unit": "Tops/s",
         "frac": achieved / int32_peak, "traffic": traffic,
-        "kernel": "ps::eval_kernel<8,int,true,false> (move-encoded search round)",
+        "kernel": "ps::eval_kernel<int, moves, smem state, derived channels, symmetric tables> (search round)",
         "kernel_ms_per_launch": 1000 * kern_s, "kernel_share_of_step": sum(kern_ms) / sum(step_ms),
-        "events_per_launch": ev_total / K, "int_ops_per_event": 10,
+        "algorithmic_events_per_launch": ev_full / K, "simulated_events_per_launch": ev_sim / K,
+        "int_ops_per_event": 10,
         "peak_source": "ps_int32_probe measured live on this GPU (IADD3/LOP3/IMAD chains)",
         "hbm": {"algorithmic_bytes_per_launch": n_cand * (16 + 20 + 8 * inst.num_stages),
                 "achieved_gbs": n_cand * (16 + 20 + 8 * inst.num_stages) / kern_s / 1e9,
                 "peak_gbs": 6536.0, "note": "not the binding roof: move-encoded candidates"},
-        "note": "latency-bound discrete-event simulation; frac is INT32 issue utilisation"}
+        "note": "latency-bound discrete-event simulation (SURVEY.md 8(d)): achieved counts the algorithmic "
+                "work of every evaluated candidate (10 int ops x its 3Pm + 2|off| events); prefix and suffix "
+                "sharing simulate only simulated_events_per_launch of them"}
 
     # ---- e2e through the C ABI with host buffers --------------------------------------------------
     if not args.no_e2e:
@@ -370,6 +405,30 @@ def main():
                                                int(gpu_ms[:n][gpu_ms[:n] >= 0].min() if (gpu_ms[:n] >= 0).any() else -1))}}
         if not args.no_e2e:
             line["e2e"]["feasible_share"] = float((e2e_flags & 1).mean())
+    # ---- time to best (BASELINE metric, second half): a fresh search from the same warm start,
+    # rounds until 16 in a row bring nothing (or the round cap), wall clock per strict improvement --
+    if not args.no_ttb:
+        ls2 = LocalSearch(inst, orders0, s0.offloaded, cfg, device=local)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        stale = 0
+        while ls2.round < args.ttb_rounds and stale < 16:
+            ls2.launch_round()
+            stale = 0 if ls2.finish_round(t0) else stale + 1
+        elapsed = time.perf_counter() - t0
+        last = ls2.improvements[-1] if ls2.improvements else None
+        ttb = {"initial_makespan": ls2.initial_makespan, "best_makespan": ls2.makespan,
+               "improvement_pct": 100.0 * (ls2.initial_makespan - ls2.makespan) / ls2.initial_makespan,
+               "rounds": ls2.round, "improvements": len(ls2.improvements),
+               "rounds_to_best": (last.round + 1) if last else 0,
+               "seconds_to_best": last.timestamp if last else 0.0, "search_seconds": elapsed,
+               "stopped_by": "16 rounds without improvement" if stale >= 16 else f"round cap {args.ttb_rounds}",
+               "neighbours_per_round": cfg.neighbours}
+        if "cpu_baseline" in line:
+            ttb["cpu_port_seconds_to_best_estimate"] = ttb["rounds_to_best"] * cfg.neighbours / line["cpu_baseline"]["value"]
+        line["time_to_best"] = ttb
     line["search"] = {"initial_makespan": ls.initial_makespan, "final_makespan": ls.makespan,
                       "warm_start": gen_name, "rounds": ls.round,
                       "improvements": [[imp.round, imp.makespan] for imp in ls.improvements]}

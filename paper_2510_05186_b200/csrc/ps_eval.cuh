@@ -616,6 +616,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             __syncwarp();
             continue;
         }
+        if (p.events_total) {
+            // the candidate's own event count: 3Pm computes and two transfers per offloaded F
+            const int n_off = __reduce_add_sync(0xffffffffu, has_stage ? cand_unrel : 0);
+            if (lane == 0) atomicAdd(p.events_total + 1, (unsigned long long)(3 * P * m + 2 * n_off));
+        }
         // ---- prefix sharing: the first step whose inputs differ from the recorded base ----
         uint32_t div = 0u;
         lastq = -1;
