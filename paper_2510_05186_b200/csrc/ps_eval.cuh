@@ -432,6 +432,10 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             p.bubble[cand] = span > 0 ? 1.0 - (double)p.busy / ((double)P * (double)span)
                                       : __longlong_as_double(0x7ff8000000000000LL);
         if (p.blocked) p.blocked[cand] = blocked_mask;
+#ifdef PS_DEBUG_EVENTS
+        // diagnostics build: simulated events | restored-from step << 16 in place of blocked
+        if (p.blocked) p.blocked[cand] = (uint32_t)(ecount - ecount0) | ((uint32_t)min(ecount0, 32767) << 16);
+#endif
     };
 
     // Checkpoint c: the state before the base commits its compute event number c*C (compute
@@ -475,6 +479,49 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 if ((SW(o_Ai + (w * 32 + __ffs(x) - 1)) & 3u) < 2u) return false;
         return true;
     };
+    // The time below which end-time word k (value w) is irrelevant: a pending reader on another
+    // resource waits for that resource's free time, which only grows, so a time at or below it
+    // (minus the comm lag) can never matter again.  INT_MAX-free: INT_MAX = no such reader.
+    // Warp-collective (shuffles): every lane calls it; `need` selects the lanes that use it.
+    auto dom_bound = [&](bool need, int k, uint32_t w) -> int {
+        const bool isA = k < P * m;
+        const int kk = isA ? k : k - P * m;
+        const int si = need ? kk / m : 0, j = need ? kk - si * m : 0;
+        const int sf_up = __shfl_sync(0xffffffffu, sfree, min(si + 1, 31));
+        const int sf_dn = __shfl_sync(0xffffffffu, sfree, max(si - 1, 0));
+        const int sf_own = __shfl_sync(0xffffffffu, sfree, si);
+        const int cf_own = __shfl_sync(0xffffffffu, cfree, si);
+        int bound = INT_MAX;
+        if (need) {
+            const uint32_t st = w & 3u;
+            if (isA && st == 1u) {          // F end: F(si+1, j), and F(si, j)'s offload
+                if (si + 1 < P && (SW(o_A + ((si + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
+                if (((SW(o_A + (2 * P * m + si * MW + (j >> 5))) >> (j & 31)) & 1u) &&
+                    (SW(o_A + (P * m + si * m + j)) & 3u) == 0u)
+                    bound = min(bound, cf_own);
+            } else if (isA) {               // B end: B(si-1, j)
+                if (si > 0 && (SW(o_A + ((si - 1) * m + j)) & 3u) < 2u) bound = min(bound, sf_dn - p.comm);
+            } else if (st == 2u) {          // reload end: B(si, j)
+                bound = min(bound, sf_own);
+            }
+        }
+        return bound;
+    };
+    // Recording: drop every such time at each checkpoint boundary, so checkpoints hold only times
+    // that still matter (simulations are unchanged; state bits are untouched, so the predicates
+    // other lanes read meanwhile are stable).
+    auto canon_dominated = [&]() {
+        const int n2 = 2 * P * m;
+        for (int k0 = 0; k0 < n2; k0 += 32) {
+            const int k = k0 + lane;
+            const uint32_t w = k < n2 ? SW(o_A + (k)) : 0u;
+            const bool timed = (w >> 2) != 0u && w != A_DEAD;
+            if (!__any_sync(0xffffffffu, timed)) continue;
+            const int bound = dom_bound(timed, k, w);
+            if (timed && bound != INT_MAX && (int)(w >> 2) <= bound) SW(o_A + (k)) = w & 3u;
+        }
+        __syncwarp();
+    };
     // Is this candidate's live state before its current step that of the base before step c*C,
     // up to one time shift `delta` of every live time (stage and channel free times, live F/B and
     // transfer end times, ledger breakpoints; usages, positions and pending sets equal)?  The
@@ -498,13 +545,23 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                  (long long)top == *reinterpret_cast<const long long *>(rg + 14);
         }
         if (!__all_sync(0xffffffffu, eq)) return false;
-        // end-time words (time << 2 | state): a word that still carries a time (> 0) must be the
-        // base's moved by delta; state-only words (time 0, dead) must be equal
+        // end-time words (time << 2 | state): a time the base's checkpoint still carries (it
+        // matters there) must be the candidate's moved by delta; a time the checkpoint dropped must
+        // be irrelevant in the candidate too (dom_bound); state-only words must be equal
         const uint32_t d4 = (uint32_t)d << 2;
-        for (int k = lane; k < 2 * P * m; k += 32) {
-            const uint32_t cw = SW(o_A + (k)), bw = src[k];
+        const int n2 = 2 * P * m;
+        for (int k0 = 0; k0 < n2; k0 += 32) {
+            const int k = k0 + lane;
+            uint32_t cw = 0u, bw = 0u;
+            if (k < n2) { cw = SW(o_A + (k)); bw = src[k]; }
             const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
-            eq = eq && (timed_c == timed_b) && (timed_c ? cw - bw == d4 : cw == bw);
+            bool ok = (timed_c == timed_b) && (timed_c ? cw - bw == d4 : cw == bw);
+            const bool relax = !ok && timed_c && !timed_b && (cw & 3u) == bw;
+            if (__any_sync(0xffffffffu, relax)) {
+                const int bound = dom_bound(relax, k, cw);
+                if (relax) ok = bound != INT_MAX && (int)(cw >> 2) <= bound;
+            }
+            eq = eq && ok;
         }
         for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
             eq = eq && SW(o_A + (k)) == src[k];
@@ -768,11 +825,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 // Suffix sharing.  A re-recording converges onto the previous base the same way:
                 // it saves this checkpoint, then stops, and the remaining ones are the previous
                 // base's shifted (rec_shift_kernel).
+                if (REC) canon_dominated();
                 if ((REC ? n_src > 1 : n_ck > 1) && cc > (int)div && c < n_src) {
                     const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead()));
-                    if (__all_sync(0xffffffffu, gate) && same_state(c)) {
-                        conv_c = c;
-                        if (!REC) break;
+                    if (__all_sync(0xffffffffu, gate)) {
+                        if (same_state(c)) {
+                            conv_c = c;
+                            if (!REC) break;
+                        }
                     }
                 }
                 // (a re-recording keeps the previous base's checkpoint it resumed from: same state)

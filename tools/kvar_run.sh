@@ -1,3 +1,3 @@
-timeout 300 python tools/prefix_diff.py 4 2>&1 | tail -1
-NCAND=256 REPS=1 timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool initcheck --print-limit 3 python tools/prefix_diff.py 2 > gpurun_out/initcheck.txt 2>&1; grep -A3 "Uninit" gpurun_out/initcheck.txt | head -12; grep "SUMMARY" gpurun_out/initcheck.txt
+PS_LIBRARY=$PWD/paper_2510_05186_b200/_lib/var/libps_dbgev.so timeout 300 python tools/event_stats.py 3 2>&1 | head -4
 timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 120 python tools/kvar.py 3
