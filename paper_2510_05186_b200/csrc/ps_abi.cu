@@ -578,7 +578,7 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
         B->ck_words = ck_u + I->P * B->K * vw + 32 * CK_REGW;
     }
     // checkpoints every ck_interval compute events (3Pm per candidate)
-    B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 16))));
+    B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 8))));
     B->ck_max = 3 * I->P * I->m / B->ck_interval + 2;
     cudaError_t e = cudaMalloc((void **)&B->ck, (size_t)B->ck_max * B->ck_words * 4);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->cstep, (size_t)I->P * I->L * 4);

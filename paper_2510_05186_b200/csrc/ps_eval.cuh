@@ -642,12 +642,51 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             return n;
         };
         int cand_unrel = 0;
+        lastq = -1;
+        int dq = L;         // first position where the row differs from the recorded base's
         if (has_stage) {
             cand_unrel = build_mask(true);
             if (!MOVES) {
-                // the stage order must be a permutation of the stage's 3m ops: 3m valid codes
-                // without a repeat (seen-sets in registers up to m = 64, else in the A row)
-                if (m <= 64) {
+                bool full = true;
+                if (n_src > 0) {
+                    // first and last position where the row differs from the (well-formed) base's,
+                    // eight codes at a time (rows are padded to a multiple of 8)
+                    const uint16_t *brow = p.base_orders + (size_t)i * p.stride;
+                    auto differs8 = [&](int q) -> bool {
+                        const uint4 a = row8(q), b = __ldg(reinterpret_cast<const uint4 *>(brow + q));
+                        return a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
+                    };
+                    int q = 0;
+                    while (q + 8 <= L && !differs8(q)) q += 8;
+                    while (q < L && row_at(i * p.stride + q) == brow[q]) ++q;
+                    dq = q;
+                    if (q < L) {
+                        int e = L - 1;          // every position above e is equal
+                        while (e > q && ((e + 1) & 7) && row_at(i * p.stride + e) == brow[e]) --e;
+                        if (((e + 1) & 7) == 0)
+                            while (e - 7 > q && !differs8(e - 7)) e -= 8;
+                        while (e > q && row_at(i * p.stride + e) == brow[e]) --e;
+                        lastq = e;
+                    }
+                    // equal to a permutation outside [dq, lastq]: a permutation iff that window holds
+                    // the base window's codes, each once
+                    if (dq == L) {
+                        full = false;
+                    } else if (lastq - dq < 16) {
+                        full = false;
+                        for (int t = dq; t <= lastq && !bad; ++t) {
+                            const uint32_t c = row_at(i * p.stride + t);
+                            bool found = false;
+                            for (int u = dq; u <= lastq; ++u) found = found || brow[u] == c;
+                            for (int u = dq; u < t; ++u) bad = bad || row_at(i * p.stride + u) == c;
+                            bad = bad || !found;
+                        }
+                    }
+                }
+                // otherwise the whole order must be a permutation of the stage's 3m ops: 3m valid
+                // codes without a repeat (seen-sets in registers up to m = 64, else in the A row)
+                if (!full) {
+                } else if (m <= 64) {
                     unsigned long long fm = 0ull, bm = 0ull, wm = 0ull;
                     for (int q = 0; q < L; ++q) {
                         const uint32_t op = row_at(i * p.stride + q), j = op >> 2, k = op & 3u;
@@ -670,6 +709,12 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
         if (__any_sync(0xffffffffu, bad)) {
             if (lane == 0) put_result(FLAG_MALFORMED, -1LL, 0u);
+            if (REC && lane == 0) {
+                // a malformed base is unusable (and must not leave the previous one's tables live)
+                p.base_info[0] = -1;
+                p.base_info[1] = (int)FLAG_MALFORMED;
+                p.base_info[5] = -1;
+            }
             __syncwarp();
             continue;
         }
@@ -680,7 +725,6 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         }
         // ---- prefix sharing: the first step whose inputs differ from the recorded base ----
         uint32_t div = 0u;
-        lastq = -1;
         eoff = 0;
         if (n_src > 0) {
             uint32_t d = NEVER;
@@ -695,26 +739,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     }
                     for (int w = 0; w < MW; ++w) nbase += __popc(base_word(w));
                 } else {
-                    // first and last position where the row differs from the base's, eight codes
-                    // at a time (rows are padded to a multiple of 8; the padding never differs
-                    // inside [0, L) bounds)
-                    const uint16_t *brow = p.base_orders + (size_t)i * p.stride;
-                    auto differs8 = [&](int q) -> bool {
-                        const uint4 a = row8(q), b = __ldg(reinterpret_cast<const uint4 *>(brow + q));
-                        return a.x != b.x || a.y != b.y || a.z != b.z || a.w != b.w;
-                    };
-                    int q = 0;
-                    while (q + 8 <= L && !differs8(q)) q += 8;
-                    while (q < L && row_at(i * p.stride + q) == brow[q]) ++q;
-                    if (q < L) {
-                        d = after(q);
-                        int e = L - 1;          // every position above e is equal
-                        while (e > q && ((e + 1) & 7) && row_at(i * p.stride + e) == brow[e]) --e;
-                        if (((e + 1) & 7) == 0)
-                            while (e - 7 > q && !differs8(e - 7)) e -= 8;
-                        while (e > q && row_at(i * p.stride + e) == brow[e]) --e;
-                        lastq = e;
-                    }
+                    if (dq < L) d = after(dq);       // (dq, lastq: found while validating)
                     for (int w = 0; w < MW; ++w) {
                         const uint32_t bb = base_word(w);
                         nbase += __popc(bb);
