@@ -160,8 +160,9 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     pl->gstate = true;
     pl->warps = 4;
     const int max_warps = std::max(1, std::min(4, env_int("PS_WARPS_PER_BLOCK", 4)));
+    const bool force_g = env_int("PS_FORCE_GSTATE", 0) != 0;     // (experiments)
     for (int w : {4, 2, 1}) {
-        if (w > max_warps) continue;
+        if (w > max_warps || force_g) continue;
         size_t smem = (size_t)(pl->inc_words + w * pl->cand_words) * 4;
         if (smem <= (size_t)I->max_smem_optin) {
             pl->warps = w;
@@ -170,8 +171,14 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
             break;
         }
     }
+    // A candidate so large that shared memory holds at most 2 per SM (config 5: 32 x 256) runs
+    // faster from L2-resident global scratch with ~12 warps per SM (22 vs 30 ms per 16,384 config-5
+    // neighbours, r01).
+    if (!pl->gstate && (size_t)(pl->inc_words + pl->warps * pl->cand_words) * 4 * 2 > (size_t)I->max_smem_optin &&
+        pl->warps <= 2 && env_int("PS_FORCE_SMEM", 0) == 0)
+        pl->gstate = true;
     if (pl->gstate) {
-        // global-memory state: one warp per block and a bounded grid keep the scratch small
+        // global-memory state: one warp per block
         pl->warps = 1;
         pl->cfg.smem = (size_t)pl->inc_words * 4;
     }
@@ -188,7 +195,8 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     if (e != cudaSuccess) return cuda_fail(e, "occupancy");
     if (per_sm < 1) per_sm = 1;
     int64_t want = (N + pl->warps - 1) / pl->warps;
-    int64_t cap = pl->gstate ? 2 * (int64_t)I->num_sms : (int64_t)per_sm * I->num_sms;
+    int64_t cap = pl->gstate ? std::min<int64_t>(per_sm, env_int("PS_GSTATE_BLOCKS_PER_SM", 16)) * I->num_sms
+                             : (int64_t)per_sm * I->num_sms;
     pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
     pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * pl->warps * pl->cand_words * 4 : 0;
     return PS_OK;

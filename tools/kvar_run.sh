@@ -1,3 +1,2 @@
-timeout 600 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 120 python tools/e2e_parts.py 2>&1 | tail -5
-timeout 300 python bench.py --no-cpu --no-ttb 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['kernel_ms_per_launch'], d['roofline']['simulated_events_per_launch'], d['e2e']['value'], d['e2e']['ms_per_step'])"
+for bps in 2 8 16; do PS_FORCE_GSTATE=1 PS_GSTATE_BLOCKS_PER_SM=$bps timeout 300 python tools/kvar.py 5 16384 2>&1 | tail -1; done
+for bps in 8 16; do PS_FORCE_GSTATE=1 PS_GSTATE_BLOCKS_PER_SM=$bps timeout 300 python tools/kvar.py 4 65536 2>&1 | tail -1; done
