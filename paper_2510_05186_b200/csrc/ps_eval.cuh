@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     V base = 0, top = 0, peak = 0;
     V segpk = 0;                               // REC: max usage folded since the last checkpoint
     int ws = 0, we = 0;
+    int wlo = INT_MAX, whi = INT_MIN;          // times of the window's first / last breakpoint
     int n_poff = 0, n_prel = 0, n_unrel = 0;   // pending offloads / reloads / offloaded not yet reloaded
     // earliest_fit cache, valid until the ledger changes; NO_R marks it empty (R >= -delta > NO_R)
     constexpr V NO_R = (V)(sizeof(V) == 8 ? (V)0x8000000000000000LL : (V)0x80000000);
@@ -270,13 +271,15 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     // holding the usage AFTER it; slots [ws, we) of a 2K array, compacted when the end is reached.
     // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
     auto win_fold = [&](int line) {
-        while (ws < we && (int)SW(o_wt + (ws)) < line) {
+        while (ws < we && wlo < line) {
             V u = SV(o_wu + (ws));
             peak = u > peak ? u : peak;
             if (REC) segpk = u > segpk ? u : segpk;
             base = u;
             ++ws;
+            wlo = ws < we ? (int)SW(o_wt + (ws)) : INT_MAX;
         }
+        if (ws == we) whi = INT_MIN;
     };
     // Called before sfree / cfree / n_unrel reflect the event being committed: the fold line is
     // below sfree, and below the channel's free time while this stage still has a transfer to come,
@@ -286,10 +289,16 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         top += d;
         rF = rG = NO_R;                                // the ledger changed: drop cached answers
         int k = we - 1;
-        while (k >= ws && (int)SW(o_wt + (k)) > t) --k;         // last breakpoint at or before t
-        if (k >= ws && (int)SW(o_wt + (k)) == t) {              // same time: merge into that breakpoint
-            for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;
+        if (ws < we && t == whi) {                     // same time as the last breakpoint: merge
+            SV(o_wu + (k)) += d;
             return;
+        }
+        if (ws < we && t < whi) {
+            while (k >= ws && (int)SW(o_wt + (k)) > t) --k;     // last breakpoint at or before t
+            if (k >= ws && (int)SW(o_wt + (k)) == t) {          // same time: merge into that breakpoint
+                for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;
+                return;
+            }
         }
         if (we - ws == K) { ovf = true; return; }
         if (we == 2 * K) {                             // compact to the front
@@ -302,6 +311,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         SW(o_wt + (k + 1)) = (uint32_t)t;
         SV(o_wu + (k + 1)) = (k >= ws ? SV(o_wu + (k)) : base) + d;
         ++we;
+        if (k + 1 == we - 1) whi = t;                  // appended
+        if (k + 1 == ws) wlo = t;                      // new first breakpoint
     };
     // earliest_fit core: first breakpoint after the last one whose usage exceeds R.
     auto win_tau = [&](V R) -> int {
@@ -787,6 +798,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
                 for (int q = 0; q < we; ++q) { SW(o_wt + (q)) = st[q]; SV(o_wu + (q)) = su[q]; }
+                wlo = we > 0 ? (int)st[0] : INT_MAX;
+                whi = we > 0 ? (int)st[we - 1] : INT_MIN;
             }
             __syncwarp();
             if (has_stage) {
@@ -814,6 +827,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             ecount0 = 0;
             pos = 0; sfree = 0; cfree = 0;
             base = top = peak = 0; ws = we = 0;
+            wlo = INT_MAX; whi = INT_MIN;
             n_poff = n_prel = 0;
             n_unrel = cand_unrel;
             first_start = INT_MAX; ecount = 0;
