@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     uint32_t head = 0, nxt = 0;
     int cpos = 0;
     uint32_t chead = NO_CHAN, cnext = NO_CHAN;
+    int wt = -1;        // see compute_key
     int lastq = -1;     // last position of this stage's order that differs from the base's
     int eoff = 0;       // base step = candidate step + eoff once the candidate's extra/missing transfers are done
 
@@ -355,8 +356,10 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         return tauG;
     };
 
+    // wt: the stage whose uncommitted op the head waits for (-1: none, or memory / a transfer)
     auto compute_key = [&]() {
         ckey = KEY_ABSENT;
+        wt = -1;
         if (pos >= L) return;
         const int j = head >> 2, k = head & 3u;
         int fl;
@@ -364,16 +367,16 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             fl = 0;
             if (i > 0) {
                 uint32_t a = SW(o_A + ((i - 1) * m + j));
-                if (!(a & 3u)) return;
+                if (!(a & 3u)) { wt = i - 1; return; }
                 fl = (int)(a >> 2) + p.comm;
             }
         } else if (k == KIND_B) {
             uint32_t a = SW(o_Ai + (j));
-            if ((a & 3u) != 1u) return;
+            if ((a & 3u) != 1u) { wt = i; return; }      // F(i, j) comes later in this stage's order
             fl = (int)(a >> 2);
             if (i < P - 1) {
                 uint32_t b = SW(o_A + ((i + 1) * m + j));
-                if ((b & 3u) < 2u) return;               // 2: B committed, 3: and W too
+                if ((b & 3u) < 2u) { wt = i + 1; return; }   // 2: B committed, 3: and W too
                 fl = max(fl, (int)(b >> 2) + p.comm);
             }
             if ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) {
@@ -383,13 +386,19 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             }
         } else {
             uint32_t a = SW(o_Ai + (j));
-            if ((a & 3u) != 2u) return;
+            if ((a & 3u) != 2u) { wt = i; return; }      // B(i, j) comes later in this stage's order
             fl = (int)(a >> 2);
         }
         int lo = max(fl, sfree);
         if (k == KIND_F) {
             int tau = tau_F(limit_i - val_of(j, 0));
-            if (tau == TAU_NONE) return;
+            if (tau == TAU_NONE) {
+                // the usage after everything committed stays too high; only this stage's pending
+                // offloads could lower it before the head commits (B/W are behind it): none left
+                // means waiting for itself
+                if (derived && n_poff == 0) wt = i;
+                return;
+            }
             if (tau != TAU_ANY) lo = max(lo, tau - proc_of(j, 0));
         }
         ckey = make_key((uint32_t)lo, ((uint32_t)i << 24) | ((uint32_t)j << 2) | (uint32_t)k);
@@ -847,9 +856,19 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         // a resumed recording starts from the previous base's widest window up to its checkpoint
         int max_win = REC && cc0 > 0 ? (int)p.ck[(size_t)(cc0 / p.ck_interval) * p.ck_words + ck_r + 9] : 0;
         int conv_c = -1;
+        bool early_dl = false;
         for (;;) {
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
             if (cdirty) { compute_key(); cdirty = false; }
+            if (!REC && !p.blocked) {
+                // Early deadlock: a stage whose head waits for an op behind itself in its own order,
+                // or two neighbours whose heads wait for each other, can never move again, so the
+                // run ends in OrderInfeasible.  Only the set of stages left would still change, and
+                // no output here reports it.
+                const int nx = __shfl_sync(0xffffffffu, wt, min(i + 1, 31));
+                const bool stuck = has_stage && ckey == KEY_ABSENT && (wt == i || (wt == i + 1 && nx == i));
+                if (__any_sync(0xffffffffu, stuck)) { early_dl = true; break; }
+            }
             if (tdirty) { transfer_key(); tdirty = false; }
             const unsigned long long key = min(ckey, tkey);
             const uint32_t kh = (uint32_t)(key >> 32);
@@ -1065,6 +1084,12 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
                 }
             }
+            __syncwarp();
+            continue;
+        }
+        if (early_dl) {
+            if (lane == 0) put_result(FLAG_DEADLOCK, -1LL, 0u);
+            if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = -1;
             __syncwarp();
             continue;
         }

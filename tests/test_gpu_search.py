@@ -121,11 +121,15 @@ def test_generators_match_reference_outputs(cuda_ok):
 def _eval_both(di, orders, masks, base):
     r0 = di.evaluate(orders, masks, peak=True)
     r1 = di.evaluate(orders, masks, peak=True, base=base)
+    # without the blocked-stage output, deadlocks may be concluded early (cyclic waits)
+    r2 = di.evaluate(orders, masks, base=base, out=di.alloc_results(int(orders.shape[0]), peak=True, blocked=False))
     import torch
     torch.cuda.synchronize()
     for f in ("flags", "makespan", "peak", "blocked"):
         a, b = getattr(r0, f).cpu().numpy(), getattr(r1, f).cpu().numpy()
         assert (a == b).all(), f
+    for f in ("flags", "makespan", "peak"):
+        assert (getattr(r0, f).cpu().numpy() == getattr(r2, f).cpu().numpy()).all(), f + " (no blocked output)"
     ok = (r0.flags.cpu().numpy() & 1) == 1
     assert (r0.bubble.cpu().numpy()[ok] == r1.bubble.cpu().numpy()[ok]).all()
     return r0
