@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto compute_key = [&]() {
         ckey = KEY_ABSENT;
         wt = -1;
-        if (pos >= L) return;
+        if (!has_stage || pos >= L) return;
         const int j = head >> 2, k = head & 3u;
         int fl;
         if (k == KIND_F) {

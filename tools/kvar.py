@@ -21,6 +21,13 @@ inst = workloads.CONFIGS[cfg_id]()
 s0, _ = best_feasible(inst)
 orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
 ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=n, shift_permille=700, max_shift=4))
+if os.environ.get("KVAR_INCUMBENT"):
+    # start from a saved incumbent (tools/ttb_profile.py ... <file.npz>) instead of the warm start
+    import numpy as np
+    z = np.load(os.environ["KVAR_INCUMBENT"])
+    ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
+    ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
+    ls.base.record(ls.inc_orders, ls.inc_mask)
 stream = torch.cuda.current_stream()
 ev = torch.zeros(1, dtype=torch.int64, device="cuda")
 ts = []

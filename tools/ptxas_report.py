@@ -2,12 +2,13 @@
 
   python tools/ptxas_report.py [ps_eval_i32_m1.cu]
 """
+import os
 import re
 import subprocess
 import sys
 from pathlib import Path
 
-ROOT = Path(__file__).resolve().parents[1]
+ROOT = Path(os.environ.get('PTXAS_ROOT') or Path(__file__).resolve().parents[1])
 src = ROOT / "paper_2510_05186_b200" / "csrc" / (sys.argv[1] if len(sys.argv) > 1 else "ps_eval_i32_m1.cu")
 cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-O3",
        "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", "-Xptxas=-v", "-I", str(ROOT / "include"),
