@@ -86,7 +86,7 @@ def test_kernel_matches_oracle_on_config_samples(cuda_ok):
     from paper_2510_05186_b200.heuristics import generator_structures
     from paper_2510_05186_b200.packing import encode_candidate, pack_instance
     rng = np.random.default_rng(7)
-    for cfg, n in ((1, 256), (2, 128), (3, 64), (4, 8)):
+    for cfg, n in ((1, 256), (2, 128), (3, 64), (4, 8), (5, 4)):
         inst = workloads.CONFIGS[cfg]()
         pk = pack_instance(inst)
         base = [encode_candidate(pk, o, f) for o, f in generator_structures(inst)]

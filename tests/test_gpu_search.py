@@ -60,6 +60,26 @@ def test_search_round_matches_cpu_round(cuda_ok):
     assert int(ls.best_key.item()) == best
 
 
+def test_search_round_matches_cpu_round_large(cuda_ok):
+    """Config 5 (32 stages x 256 microbatches; state in global scratch): a round's neighbours
+    with prefix/suffix sharing against the recorded incumbent vs the CPU restatement."""
+    import torch
+    from oracle.oracle import Oracle
+    inst, orders, off, LocalSearch, SearchConfig = _setup(5)
+    n = 24
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    ms = torch.empty(n, dtype=torch.int64, device="cuda")
+    ls.launch_round(ms)
+    torch.cuda.synchronize()
+    orc = Oracle(ls.di.packed)
+    best, want = orc.search_round(ls.inc_orders.cpu().numpy().view(np.uint16),
+                                  ls.inc_mask.cpu().numpy().view(np.uint32), SEED, PERMILLE, MAXSHIFT,
+                                  0, 0, n, want_makespans=True)
+    assert (ms.cpu().numpy() == want).all()
+    assert int(ls.best_key.item()) == best
+
+
 def test_identical_best_schedule_for_equal_budgets(cuda_ok):
     """A whole search: the GPU and the CPU restatement adopt the same moves and end identical."""
     from oracle.oracle import Oracle
