@@ -341,14 +341,15 @@ def main():
         outs = dict(makespan=torch.empty(n_cand, dtype=torch.int64, pin_memory=True),
                     bubble=torch.empty(n_cand, dtype=torch.float64, pin_memory=True),
                     flags=torch.empty(n_cand, dtype=torch.int32, pin_memory=True),
-                    peak=torch.empty((n_cand, pk.num_stages), dtype=torch.int64, pin_memory=True),
-                    blocked=torch.empty(n_cand, dtype=torch.int32, pin_memory=True))
+                    peak=torch.empty((n_cand, pk.num_stages), dtype=torch.int64, pin_memory=True))
+        # the search's outputs (makespan, bubble, STRICT peaks, flags) — no OrderInfeasible stage
+        # sets, which no caller of a batch needs and which let deadlocks be concluded early
         cb = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0,
                          ls.base.handle if ls.base is not None else None, 1 if u8 else 2)
         rb = N.ResultBatch(outs["makespan"].data_ptr(), outs["bubble"].data_ptr(), outs["peak"].data_ptr(),
-                           outs["flags"].data_ptr(), outs["blocked"].data_ptr(), None, None, 0, None)
+                           outs["flags"].data_ptr(), None, None, None, 0, None)
         h2d = h_orders.numel() * h_orders.element_size() + h_masks.numel() * 4
-        d2h = n_cand * (8 + 8 + 4 + 4 + 8 * pk.num_stages)
+        d2h = n_cand * (8 + 8 + 4 + 8 * pk.num_stages)
         for _ in range(args.warmup):
             N.check(lib.ps_eval_batch_host(di.handle, C.byref(cb), C.byref(rb), C.c_void_p(stream.cuda_stream)))
         if world > 1:
@@ -366,7 +367,8 @@ def main():
         e_s = float(e_tot.item()) / 1e3
         line["e2e"] = {"value": n_cand * world * K / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * e_s / K,
-                       "api": "ps_eval_batch_host (pinned host buffers, copies inside the call)"}
+                       "api": "ps_eval_batch_host (pinned host buffers, copies inside the call)",
+                       "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate"}
         e2e_flags = outs["flags"].numpy().copy()
         e2e_span = outs["makespan"].numpy().copy()
     else:

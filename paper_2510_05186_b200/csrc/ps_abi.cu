@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -29,6 +30,9 @@ struct ps_instance {
     void *d_limit;
     int32_t *d_chan;
     std::vector<uint8_t> h_offloadable;   // [P][m]
+    // occupancy answers per launch shape (the query costs microseconds per call otherwise)
+    mutable std::mutex occ_mu;
+    mutable std::map<uint64_t, int> occ_cache;
 };
 
 struct ps_base {
@@ -191,8 +195,19 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     v.record = false;
     v.derived = true;
     v.uni = I->uniform != 0;
-    cudaError_t e = occupancy(I->v64, moves, v, pl->cfg.block, pl->cfg.smem, &per_sm);
-    if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+    const uint64_t okey = ((uint64_t)pl->cfg.smem << 16) | ((uint64_t)pl->cfg.block << 2) |
+                          ((uint64_t)pl->gstate << 1) | (uint64_t)moves;
+    {
+        std::lock_guard<std::mutex> lk(I->occ_mu);
+        auto it = I->occ_cache.find(okey);
+        if (it != I->occ_cache.end()) per_sm = it->second;
+    }
+    if (per_sm == 0) {
+        cudaError_t e = occupancy(I->v64, moves, v, pl->cfg.block, pl->cfg.smem, &per_sm);
+        if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+        std::lock_guard<std::mutex> lk(I->occ_mu);
+        I->occ_cache[okey] = per_sm > 0 ? per_sm : 1;
+    }
     if (per_sm < 1) per_sm = 1;
     int64_t want = (N + pl->warps - 1) / pl->warps;
     int64_t cap = pl->gstate ? std::min<int64_t>(per_sm, env_int("PS_GSTATE_BLOCKS_PER_SM", 16)) * I->num_sms
@@ -815,11 +830,17 @@ int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_re
     PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
     int32_t *ready = (int32_t *)(arena + off[3]);
     PS_CUDA(cudaMemsetAsync(ready, 0, (size_t)nchunks * 4, s));
-    cudaStream_t cs = nullptr;
-    cudaEvent_t ev_start = nullptr, ev_copied = nullptr;
-    PS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    PS_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-    PS_CUDA(cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming));
+    // the copy stream and its two events are kept per thread and device
+    struct CopyRes { cudaStream_t cs = nullptr; cudaEvent_t start = nullptr, copied = nullptr; };
+    static thread_local std::map<int, CopyRes> copy_res;
+    CopyRes &cr = copy_res[I->device];
+    if (!cr.cs) {
+        PS_CUDA(cudaStreamCreateWithFlags(&cr.cs, cudaStreamNonBlocking));
+        PS_CUDA(cudaEventCreateWithFlags(&cr.start, cudaEventDisableTiming));
+        PS_CUDA(cudaEventCreateWithFlags(&cr.copied, cudaEventDisableTiming));
+    }
+    cudaStream_t cs = cr.cs;
+    cudaEvent_t ev_start = cr.start, ev_copied = cr.copied;
     PS_CUDA(cudaEventRecord(ev_start, s));                  // arena and cleared flags exist
     PS_CUDA(cudaStreamWaitEvent(cs, ev_start, 0));
     // every copy is enqueued before the evaluation launches: the flags it waits for are certain
@@ -865,9 +886,6 @@ int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_re
     cudaFreeAsync(arena, s);
     cudaError_t e = cudaStreamSynchronize(s);
     cudaStreamSynchronize(cs);
-    cudaEventDestroy(ev_start);
-    cudaEventDestroy(ev_copied);
-    cudaStreamDestroy(cs);
     if (rc) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "ps_eval_batch_host");
     return PS_OK;

@@ -1,13 +1,37 @@
 // ps_eval_impl.cuh — instantiation helpers for ps_launch.h (included once per (V, MOVES) TU).
 #pragma once
+#include <atomic>
 #include "ps_launch.h"
 
 namespace ps {
 
+// Raise a kernel's dynamic shared-memory limit only when a launch needs more than was already
+// granted on this device (the attribute call costs microseconds on every launch otherwise).
+template <typename Fn>
+static cudaError_t ensure_smem(Fn fn, size_t smem, std::atomic<int> *granted) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::atomic<int> &g = granted[dev & 63];
+    if ((int)smem <= g.load(std::memory_order_relaxed)) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int cur = g.load();
+    while ((int)smem > cur && !g.compare_exchange_weak(cur, (int)smem)) {}
+    return cudaSuccess;
+}
+
+// one grant record per kernel instantiation and device, shared by launches and occupancy queries
+template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
+static std::atomic<int> *granted_for() {
+    static std::atomic<int> g[64];
+    return g;
+}
+
 template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
 static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t stream) {
     auto fn = eval_kernel<V, MOVES, GSTATE, REC, DERIVED, UNI>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem);
+    cudaError_t e = ensure_smem(fn, cfg.smem, granted_for<V, MOVES, GSTATE, REC, DERIVED, UNI>());
     if (e != cudaSuccess) return e;
     fn<<<cfg.grid, cfg.block, cfg.smem, stream>>>(p);
     return cudaGetLastError();
@@ -16,7 +40,7 @@ static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t s
 template <typename V, bool MOVES, bool GSTATE, bool DERIVED, bool UNI>
 static cudaError_t occ_one(int block, size_t smem, int *n) {
     auto fn = eval_kernel<V, MOVES, GSTATE, false, DERIVED, UNI>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_smem(fn, smem, granted_for<V, MOVES, GSTATE, false, DERIVED, UNI>());
     if (e != cudaSuccess) return e;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, fn, block, smem);
 }

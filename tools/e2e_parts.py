@@ -40,5 +40,17 @@ print("h2d 8-bit orders  ms", t(lambda: dev8.copy_(h8, non_blocking=True)), "byt
 print("eval device u8    ms", t(lambda: ls.di.evaluate(od8, md, peak=True, base=ls.base)))
 print("eval device u16   ms", t(lambda: ls.di.evaluate(od, md, peak=True, base=ls.base)))
 print("eval device nobase ms", t(lambda: ls.di.evaluate(od8, md, peak=True)))
+import numpy as np
 ho, hmm = h8.numpy(), hm.numpy()
 print("eval host u8      ms", t(lambda: ls.di.evaluate_host(ho, hmm, peak=True, base=ls.base)))
+import ctypes as C  # noqa: E402
+from paper_2510_05186_b200 import _native as N  # noqa: E402
+pk = ls.di.packed
+for nn in (64, 4096, 65536):
+    hs = ho[:nn].copy() if nn < n else ho
+    out = dict(ms=np.empty(nn, np.int64), bb=np.empty(nn, np.float64), fl=np.empty(nn, np.int32), pk=np.empty((nn, pk.num_stages), np.int64))
+    hmm2 = hmm[:nn].copy() if nn < n else hmm
+    cb = N.CandBatch(nn, hs.ctypes.data, hmm2.ctypes.data, None, 0, ls.base.handle, 1)
+    rb = N.ResultBatch(out["ms"].ctypes.data, out["bb"].ctypes.data, out["pk"].ctypes.data, out["fl"].ctypes.data, None, None, None, 0, None)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    print("host call N=%d (numpy pageable, no blocked)" % nn, "ms", t(lambda: N.check(ls.lib.ps_eval_batch_host(ls.di.handle, C.byref(cb), C.byref(rb), st))))
