@@ -136,6 +136,14 @@ typedef struct ps_search_desc {
     const ps_base *base;            /* optional: the incumbent recorded with ps_base_record        */
 } ps_search_desc;
 
+/* A batch of branch-and-bound nodes (device buffers): the state solver._Search._bound reads. */
+typedef struct ps_bound_batch {
+    int64_t num_nodes;
+    const int32_t *clock;           /* [N] node clock                                              */
+    const int32_t *stage_free;      /* [N][P] stage free times                                     */
+    const int32_t *comp_start;      /* [N][P][m][3] committed compute starts (F, B, W), -1 = not   */
+} ps_bound_batch;
+
 const char *ps_version(void);
 const char *ps_last_error(void);
 
@@ -158,6 +166,10 @@ int ps_base_record(ps_base *base, const uint16_t *orders, const uint32_t *mask, 
 enum { PS_BASE_CHECKPOINTS = 0, PS_BASE_CSTEP = 1, PS_BASE_FSTEP = 2, PS_BASE_INFO = 3, PS_BASE_RESULT = 4,
        PS_BASE_LAYOUT = 5 };
 int ps_base_read(const ps_base *base, int what, void *host, size_t *bytes);
+
+/* Lower bound of every node in the batch, one warp per node: replaces solver._Search._bound
+   (solver.py:352-383) with _chain_ends (solver.py:321-350), bit-exact (int64 out, device [N]). */
+int ps_bound_batch_eval(const ps_instance *inst, const ps_bound_batch *batch, int64_t *lower_bound, void *stream);
 
 /* Evaluate N candidates (device buffers) on `stream` (a cudaStream_t, NULL = legacy default). */
 int ps_eval_batch(const ps_instance *inst, const ps_cand_batch *batch,

@@ -66,6 +66,8 @@ def lib():
                                          C.POINTER(_Moves), C.c_uint64, C.c_int64, C.c_int64,
                                          C.c_void_p, C.c_int32]
         _lib.or_search_round.restype = C.c_int64
+        _lib.or_bound.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32]
+        _lib.or_bound.restype = C.c_int64
     return _lib
 
 
@@ -141,6 +143,13 @@ class Oracle:
                                         inc_m.ctypes.data, C.byref(mv), rnd, first, count,
                                         ms.ctypes.data if ms is not None else None, int(threads))
         return best, ms
+
+
+def bound(orc: "Oracle", t, sfree, start, post) -> int:
+    """B&B node lower bound (solver.py:321-383); start [P][m][3] int64 with -1 = uncommitted."""
+    sf = np.ascontiguousarray(sfree, np.int64)
+    st = np.ascontiguousarray(start, np.int64)
+    return int(orc.lib.or_bound(C.byref(orc._inst), int(t), sf.ctypes.data, st.ctypes.data, int(bool(post))))
 
 
 def philox4x32_10(ctr, key):

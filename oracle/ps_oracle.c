@@ -586,3 +586,85 @@ int64_t or_search_round(const or_instance *I, const uint16_t *inc, int32_t strid
     pthread_mutex_destroy(&s.mu);
     return s.best;
 }
+
+/* ---- B&B node lower bound: solver._Search._bound (solver.py:352-383) with _chain_ends
+ * (solver.py:321-350), restated over dense tables.  start[(i*m + j)*3 + k] is the committed start
+ * of op (i, j, k) or -1; sfree[i] the stage free time; t the node's clock. */
+int64_t or_bound(const or_instance *I, int64_t t, const int64_t *sfree, const int64_t *start, int32_t post) {
+    const int P = I->P, m = I->m;
+#define ST(i, j, k) start[((size_t)(i) * m + (j)) * 3 + (k)]
+#define PT(i, j, k) I->proc[((size_t)(i) * m + (j)) * 3 + (k)]
+    if (post) {                                                    /* solver.py:354-369 */
+        int64_t worst = 0;
+        for (int i = 0; i < P; ++i) {
+            int64_t rem = 0, first_f = INT64_MAX, last_w = INT64_MIN;
+            int have_f = 0;
+            for (int j = 0; j < m; ++j)
+                for (int k = 0; k < 3; ++k) {
+                    if (ST(i, j, k) < 0) { rem += PT(i, j, k); continue; }
+                    if (k == 0) { have_f = 1; if (ST(i, j, 0) < first_f) first_f = ST(i, j, 0); }
+                    if (k == 2 && ST(i, j, 2) + PT(i, j, 2) > last_w) last_w = ST(i, j, 2) + PT(i, j, 2);
+                }
+            int64_t v;
+            if (rem == 0) v = last_w - first_f;
+            else if (have_f) v = (sfree[i] > t ? sfree[i] : t) + rem - first_f;
+            else v = rem;
+            if (v > worst) worst = v;
+        }
+        return worst;
+    }
+    int64_t lb = 0, min_start = INT64_MAX;                         /* solver.py:370-383 */
+    int any = 0;
+    for (int i = 0; i < P; ++i)
+        for (int j = 0; j < m; ++j)
+            for (int k = 0; k < 3; ++k)
+                if (ST(i, j, k) >= 0) {
+                    any = 1;
+                    if (ST(i, j, k) + PT(i, j, k) > lb) lb = ST(i, j, k) + PT(i, j, k);
+                    if (ST(i, j, k) < min_start) min_start = ST(i, j, k);
+                }
+    for (int i = 0; i < P; ++i) {
+        int64_t rem = 0;
+        for (int j = 0; j < m; ++j)
+            for (int k = 0; k < 3; ++k)
+                if (ST(i, j, k) < 0) rem += PT(i, j, k);
+        if (rem) {
+            int64_t v = (sfree[i] > t ? sfree[i] : t) + rem;
+            if (v > lb) lb = v;
+        }
+    }
+    /* _chain_ends: F down the stages, then B up the stages with each W after its B */
+    int64_t *E = (int64_t *)malloc(sizeof(int64_t) * (size_t)P * m * 3);
+#define EE(i, j, k) E[((size_t)(i) * m + (j)) * 3 + (k)]
+    for (int j = 0; j < m; ++j)
+        for (int i = 0; i < P; ++i) {
+            if (ST(i, j, 0) >= 0) { EE(i, j, 0) = ST(i, j, 0) + PT(i, j, 0); continue; }
+            int64_t lo = sfree[i] > t ? sfree[i] : t;
+            if (i > 0 && EE(i - 1, j, 0) + I->comm > lo) lo = EE(i - 1, j, 0) + I->comm;
+            EE(i, j, 0) = lo + PT(i, j, 0);
+        }
+    for (int j = 0; j < m; ++j)
+        for (int i = P - 1; i >= 0; --i) {
+            if (ST(i, j, 1) >= 0) EE(i, j, 1) = ST(i, j, 1) + PT(i, j, 1);
+            else {
+                int64_t lo = sfree[i] > t ? sfree[i] : t;
+                if (EE(i, j, 0) > lo) lo = EE(i, j, 0);
+                if (i < P - 1 && EE(i + 1, j, 1) + I->comm > lo) lo = EE(i + 1, j, 1) + I->comm;
+                EE(i, j, 1) = lo + PT(i, j, 1);
+            }
+            if (ST(i, j, 2) >= 0) EE(i, j, 2) = ST(i, j, 2) + PT(i, j, 2);
+            else {
+                int64_t lo = sfree[i] > t ? sfree[i] : t;
+                if (EE(i, j, 1) > lo) lo = EE(i, j, 1);
+                EE(i, j, 2) = lo + PT(i, j, 2);
+            }
+        }
+    for (size_t q = 0; q < (size_t)P * m * 3; ++q)
+        if (E[q] > lb) lb = E[q];
+    free(E);
+    if (any) lb -= min_start;
+    return lb;
+#undef EE
+#undef ST
+#undef PT
+}

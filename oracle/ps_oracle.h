@@ -78,6 +78,10 @@ int64_t or_search_round(const or_instance *I, const uint16_t *inc_orders, int32_
                         const uint32_t *inc_mask, const or_moves *mv, uint64_t round, int64_t first,
                         int64_t count, int64_t *makespans, int32_t threads);
 
+/* B&B node lower bound (solver.py:321-383): start [P][m][3] committed compute starts (-1 = not
+   committed), sfree [P] stage free times, t the node clock, post the post-validation flag. */
+int64_t or_bound(const or_instance *I, int64_t t, const int64_t *sfree, const int64_t *start, int32_t post);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,15 @@ class SearchDesc(C.Structure):
     ]
 
 
+class BoundBatch(C.Structure):
+    _fields_ = [
+        ("num_nodes", C.c_int64),
+        ("clock", C.c_void_p),
+        ("stage_free", C.c_void_p),
+        ("comp_start", C.c_void_p),
+    ]
+
+
 EXPORTS = {
     "ps_version": (C.c_char_p, []),
     "ps_last_error": (C.c_char_p, []),
@@ -131,6 +140,7 @@ EXPORTS = {
     "ps_base_destroy": (C.c_int, [C.c_void_p]),
     "ps_base_record": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ps_base_read": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_size_t)]),
+    "ps_bound_batch_eval": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

@@ -891,6 +891,23 @@ int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_re
     return PS_OK;
 }
 
+extern "C" cudaError_t ps_bound_launch(int P, int m, int uniform, int post, int comm, const int32_t *proc, int64_t N,
+                            const int32_t *clock, const int32_t *sfree, const int32_t *start, int64_t *lb,
+                            int num_sms, cudaStream_t s);
+
+int ps_bound_batch_eval(const ps_instance *I, const ps_bound_batch *b, int64_t *lower_bound, void *stream) {
+    if (!I || !b || !lower_bound) return fail(PS_ERR_INVALID, "null argument");
+    if (b->num_nodes < 0) return fail(PS_ERR_INVALID, "negative node count");
+    if (b->num_nodes == 0) return PS_OK;
+    if (!b->clock || !b->stage_free || !b->comp_start) return fail(PS_ERR_INVALID, "clock, stage_free and comp_start are required");
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaError_t e = ps_bound_launch(I->P, I->m, I->uniform, I->post, I->comm, I->d_proc, b->num_nodes, b->clock,
+                                    b->stage_free, b->comp_start, lower_bound, I->num_sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "bound launch");
+    return PS_OK;
+}
+
 int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
                     void *stream) {
     if (!I || !d || !best_key) return fail(PS_ERR_INVALID, "null argument");

@@ -60,3 +60,28 @@ def test_malformed_candidates_are_flagged():
     bad = orders.copy()
     bad[0, 1] = bad[0, 0]          # duplicate op
     assert orc.run(bad, mask)["flags"] == 4
+
+
+def test_bound_restatement_matches_reference_solver():
+    """or_bound (the C restatement of solver.py:321-383) equals the bound the reference solver
+    computed at every recorded node (tests/golden/bounds.json.gz, make_bound_golden.py)."""
+    import gzip
+    import json
+    from pathlib import Path
+    import numpy as np
+    from oracle.oracle import Oracle, bound
+    from paper_2510_05186_b200.instance import instance_from_dict
+    from paper_2510_05186_b200.packing import pack_instance
+    d = json.load(gzip.open(Path(__file__).parent / "golden" / "bounds.json.gz", "rt"))
+    n = 0
+    for r in d["rows"]:
+        pk = pack_instance(instance_from_dict(r["instance"]))
+        orc = Oracle(pk)
+        P, m = pk.num_stages, pk.num_microbatches
+        for node in r["nodes"]:
+            st = np.full((P, m, 3), -1, np.int64)
+            for i, j, k, s in node["comp"]:
+                st[i - 1, j - 1, k] = s
+            assert bound(orc, node["t"], node["sfree"], st, r["post"]) == node["lb"]
+            n += 1
+    assert n > 5000
