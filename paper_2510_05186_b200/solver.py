@@ -87,17 +87,15 @@ def incumbent_stream(session: SolveSession):
     return session.stream()
 
 
-def lower_bound(inst: PipelineInstance, post_validation: bool) -> int:
-    """Valid makespan lower bound: every stage runs its 3m ops one at a time; without
-    post-validation a microbatch's F chain down, B chain up and stage 1's W are sequential."""
-    P, m = inst.num_stages, inst.num_microbatches
-    busiest = max(sum(inst.proc_time[op] for op in inst.stage_ops(i)) for i in range(1, P + 1))
-    if post_validation:
-        return busiest
-    chain = max(sum(inst.proc_time[OpId(i, j, OpKind.F)] + inst.proc_time[OpId(i, j, OpKind.B)]
-                    for i in range(1, P + 1)) + 2 * (P - 1) * inst.comm_time
-                + inst.proc_time[OpId(1, j, OpKind.W)] for j in range(1, m + 1))
-    return max(busiest, chain)
+def lower_bound(inst: PipelineInstance, post_validation: bool, device=None) -> int:
+    """The reference solver's root bound (solver.py:481): ``_Search._bound`` at the empty node
+    (clock 0, every stage free at 0, nothing committed), computed by the batched GPU bound kernel
+    (bound.py) — per-stage work, and the F-down / B-up / W chains of every microbatch."""
+    from .bound import lower_bounds
+    if post_validation != inst.post_validation:
+        inst = replace(inst, post_validation=post_validation)
+    root = (0, {i: 0 for i in range(1, inst.num_stages + 1)}, {})
+    return lower_bounds(inst, [root], device=device)[0]
 
 
 def start_session(inst: PipelineInstance, budget: SolveBudget | None = None,
@@ -120,7 +118,7 @@ def start_session(inst: PipelineInstance, budget: SolveBudget | None = None,
             warm = None
     if warm is not None and not validate(warm, inst, MemorySemantics.STRICT).ok:
         warm = None                # unsafe warm starts are unusable as incumbents (solver.py:557-560)
-    lb = lower_bound(inst, post)
+    lb = lower_bound(inst, post, device=device)
     if warm is None:
         outcome = SolveOutcome(None, None, lb, UNKNOWN, elapsed=_time.monotonic() - t0)
         return SolveSession(outcome, [])

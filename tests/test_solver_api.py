@@ -5,7 +5,26 @@ import pytest
 from _golden import CORPORA, corpus
 
 
-def test_lower_bound_is_valid_on_every_reference_schedule():
+@pytest.mark.gpu
+def test_lower_bound_is_the_reference_root_bound(cuda_ok):
+    """lower_bound == the reference solver's root bound (the first node it bounds, solver.py:481)."""
+    import gzip
+    import json
+    from pathlib import Path
+    from paper_2510_05186_b200.instance import instance_from_dict
+    from paper_2510_05186_b200.solver import lower_bound
+    d = json.load(gzip.open(Path(__file__).parent / "golden" / "bounds.json.gz", "rt"))
+    n = 0
+    for r in d["rows"]:
+        root = r["nodes"][0]
+        assert root["t"] == 0 and not root["comp"]
+        assert lower_bound(instance_from_dict(r["instance"]), r["post"]) == root["lb"]
+        n += 1
+    assert n >= 20
+
+
+@pytest.mark.gpu
+def test_lower_bound_is_valid_on_every_reference_schedule(cuda_ok):
     from paper_2510_05186_b200.solver import lower_bound
     checked = 0
     for name in CORPORA:
