@@ -385,6 +385,8 @@ __global__ void rec_shift_kernel(RecShift r) {
         if (nb < 32) bits &= (1u << nb) - 1u;
         ck[2 * r.P * r.m + k] = bits;
     }
+    // the event step is a warp-wide scalar: every lane's copy moves
+    for (int l = threadIdx.x; l < 32; l += blockDim.x) ck[r.ck_r + l * ps::CK_REGW + 20] -= (uint32_t)r.info[7];
     const uint32_t *rg0 = r.ck + (size_t)c0 * r.ck_words + r.ck_r;
     for (int s = threadIdx.x; s < r.P; s += blockDim.x) {
         uint32_t *rg = ck + r.ck_r + s * ps::CK_REGW;
@@ -395,7 +397,6 @@ __global__ void rec_shift_kernel(RecShift r) {
         const int fs0 = (int)rg0[s * ps::CK_REGW + 8];
         if (fs0 != INT_MAX) rg[8] = (uint32_t)fs0;
         else if ((int)rg[8] != INT_MAX) rg[8] += (uint32_t)dl;
-        rg[20] -= (uint32_t)r.info[7];          // event step: the transfers differ by eoff
         long long pk = *reinterpret_cast<const long long *>(rg0 + s * ps::CK_REGW + 16);
         for (int k = c0 + 1; k <= c; ++k) {
             const long long sg = *reinterpret_cast<const long long *>(r.ck + (size_t)k * r.ck_words + r.ck_r + s * ps::CK_REGW + 10);

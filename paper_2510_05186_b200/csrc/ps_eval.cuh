@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                     }
                 }
             }
-            ecount = (int)src[ck_r + lane * CK_REGW + 20];
+            ecount = (int)src[ck_r + 20];               // (lane 0's copy: warp-uniform by construction)
             ecount0 = ecount;
             cc = ck_idx * p.ck_interval;
         } else {
@@ -860,13 +860,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         for (;;) {
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
             if (cdirty) { compute_key(); cdirty = false; }
-            if (!REC && !p.blocked) {
+            if (!REC && !p.blocked && (ecount & 3) == 0) {
                 // Early deadlock: a stage whose head waits for an op behind itself in its own order,
                 // or two neighbours whose heads wait for each other, can never move again, so the
                 // run ends in OrderInfeasible.  Only the set of stages left would still change, and
-                // no output here reports it.
+                // no output here reports it.  (Checked every 4th event: a wait, once permanent,
+                // stays so.)
                 const int nx = __shfl_sync(0xffffffffu, wt, min(i + 1, 31));
-                const bool stuck = has_stage && ckey == KEY_ABSENT && (wt == i || (wt == i + 1 && nx == i));
+                const bool stuck = wt == i || (wt == i + 1 && nx == i);      // (wt >= 0: no key)
                 if (__any_sync(0xffffffffu, stuck)) { early_dl = true; break; }
             }
             if (tdirty) { transfer_key(); tdirty = false; }

@@ -230,7 +230,9 @@ def _base_tables(base, P, m, MW):
         regs = w[ck_r:ck_r + regw * P].reshape(P, regw)
         win = [(w[ck_t + s * kc: ck_t + s * kc + regs[s, 4]].tolist(),
                 w[ck_u + s * kc: ck_u + s * kc + regs[s, 4]].tolist()) for s in range(P)]
-        cks.append((w[:nz].tolist(), regs[:, list(range(9)) + list(range(10, 21))].tolist(), win))
+        # word 20 (the event step) is warp-wide: every lane's copy, not just the stage lanes'
+        steps = w[ck_r:ck_r + regw * 32].reshape(32, regw)[:, 20].tolist()
+        cks.append((w[:nz].tolist(), regs[:, list(range(9)) + list(range(10, 21))].tolist(), win, steps))
     return info[[0, 1, 2, 3]].tolist(), res.tolist(), cstep.tolist(), fstep.tolist(), cks
 
 
@@ -260,6 +262,20 @@ def test_rerecording_equals_fresh_recording(cuda_ok, cfg):
         again.record(ls.inc_orders, ls.inc_mask)
         again.record(o[idx], mk[idx])
         assert _base_tables(fresh, P, m, MW) == _base_tables(again, P, m, MW), idx
+
+
+@pytest.mark.timeout(300)
+def test_long_search_with_converging_rerecordings(cuda_ok):
+    """Forty rounds on config 3: every improvement re-records the base, most by converging onto
+    the previous one and shifting its checkpoints; candidates then resume from shifted ones.  The
+    search must run through and end on a valid schedule with the makespan it reports."""
+    from paper_2510_05186_b200 import makespan, validate
+    inst, orders, off, LocalSearch, SearchConfig = _setup(3)
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=8192, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    res = ls.run(rounds=40)
+    assert len(res.improvements) >= 10
+    assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == res.makespan
 
 
 def test_host_buffer_path_matches_device_path(cuda_ok):
