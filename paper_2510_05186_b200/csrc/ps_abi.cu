@@ -1,5 +1,6 @@
 // ps_abi.cu — C ABI (include/pipesched_b200.h): instance tables, launch planning, search kernels.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -242,6 +243,8 @@ void attach_base(const ps_base *B, EvalParams *p) {
 // K1, then a shared-memory pass with a 4x wider window over the candidates whose ledger did not
 // fit, then a pass with the whole 5m-point ledger (cannot overflow) over what is left.  Every pass
 // reads its worklist from device memory: no host round trip.
+int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *order, cudaStream_t s);
+
 int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr) {
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
@@ -263,6 +266,14 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
     PS_CUDA(cudaMemsetAsync(lists + list_words, 0, sizeof(int32_t), s));
     PS_CUDA(cudaMemsetAsync(lists + 2 * list_words, 0, 4 * sizeof(int32_t), s));
     const bool dynamic = env_int("PS_DYNAMIC", 1) != 0;
+    // Neighbours that diverge from the base early simulate the most: the first pass takes them
+    // first (longest-processing-time order), so the round does not end on a few long stragglers.
+    int32_t *order = nullptr;
+    if (moves && p.ck && dynamic && env_int("PS_ORDER", 1) != 0) {
+        PS_CUDA(cudaMallocAsync((void **)&order, list_words * sizeof(int32_t), s));
+        int rc = order_by_divergence(I, p, order, s);
+        if (rc) return rc;
+    }
     for (int k = 0; k < npass; ++k) {
         Plan pl;
         int rc = plan_pass(I, moves, Ks[k], p.N, &pl, p.order_u8 ? 1 : 2);
@@ -271,7 +282,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.K = pl.K;
         q.cand_words = pl.cand_words;
         q.inc_words = pl.inc_words;
-        int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : nullptr;       // handoff k-1
+        int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order;         // handoff k-1
         int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
         q.work_count = in;
         q.work_list = in ? in + 1 : nullptr;
@@ -287,6 +298,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         if (scratch) PS_CUDA(cudaFreeAsync(scratch, s));
     }
     PS_CUDA(cudaFreeAsync(lists, s));
+    if (order) PS_CUDA(cudaFreeAsync(order, s));
     return PS_OK;
 }
 
@@ -404,6 +416,54 @@ __global__ void rec_shift_kernel(RecShift r) {
         }
         *reinterpret_cast<long long *>(rg + 16) = pk;
     }
+}
+
+// Divergence step of every neighbour of a round (the base's compute index before which the
+// neighbour's inputs first differ; NEVER for no-ops), with its index, for the LPT ordering.
+MoveCtx move_ctx(const ps_instance *I);
+
+__global__ void divergence_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first, int64_t count,
+                                  const uint32_t *cstep, const uint32_t *fstep, uint32_t *key, int32_t *idx,
+                                  int32_t *order_count) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n == 0) *order_count = (int32_t)count;
+    if (n >= count) return;
+    const Move mv = ctx_decode(c, mp, round, (uint64_t)(first + n));
+    uint32_t d = ps::NEVER;
+    if (mv.type == MOVE_SHIFT) {
+        const int q = mv.a < mv.b ? mv.a : mv.b;
+        d = q == 0 ? 0u : cstep[mv.stage * c.L + q - 1];
+    } else if (mv.type == MOVE_TOGGLE) {
+        d = fstep[mv.stage * c.m + mv.mb];
+    }
+    key[n] = d;
+    idx[n] = (int32_t)n;
+}
+
+int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *order, cudaStream_t s) {
+    const int64_t N = p.N;
+    uint32_t *keys = nullptr, *keys_out = nullptr;
+    int32_t *idx = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    PS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, 32, s));
+    PS_CUDA(cudaMallocAsync((void **)&keys, (size_t)N * 4, s));
+    PS_CUDA(cudaMallocAsync((void **)&keys_out, (size_t)N * 4, s));
+    PS_CUDA(cudaMallocAsync((void **)&idx, (size_t)N * 4, s));
+    PS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
+    ps_move_params mp;
+    mp.seed = p.seed;
+    mp.shift_permille = p.shift_permille;
+    mp.max_shift = p.max_shift;
+    divergence_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N,
+                                                                 p.cstep, p.fstep, keys, idx, order);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, 32, s));
+    cudaFreeAsync(keys, s);
+    cudaFreeAsync(keys_out, s);
+    cudaFreeAsync(idx, s);
+    cudaFreeAsync(tmp, s);
+    return PS_OK;
 }
 
 // Independent IADD3/LOP3/IMAD chains: the INT32 issue ceiling of the roofline.
