@@ -145,11 +145,13 @@ def build_incumbent_oracle(inst, pk, orc):
 
 
 def calibrate_sample(orc, inc_o, inc_m, rnd, threads, target_s, cap):
-    """Neighbour count whose CPU evaluation takes about target_s seconds on `threads` threads."""
+    """Neighbour count whose CPU evaluation takes about target_s seconds on `threads` threads
+    (timed on a sample of 8 candidates per thread: per-candidate costs vary several-fold)."""
+    k = min(cap, 8 * threads)
     t = time.perf_counter()
-    orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"], rnd, 0, threads, threads)
-    per = (time.perf_counter() - t) / max(1, threads)     # seconds per candidate-thread
-    n = int(target_s / max(per, 1e-6) * threads)
+    orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"], rnd, 0, k, threads)
+    per = (time.perf_counter() - t) / k                   # wall seconds per candidate, all threads
+    n = int(target_s / max(per, 1e-7))
     return max(threads, min(cap, n))
 
 
@@ -166,9 +168,15 @@ def run_reference(args):
     orc = Oracle(pk)
     threads = cpu_threads()
     inc_o, inc_m, _ = build_incumbent_oracle(inst, pk, orc)
-    n = calibrate_sample(orc, inc_o, inc_m, 0, threads, args.ref_step_seconds, PER_GPU * max(1, args.gpus))
+    # each step a bounded sample: the whole --steps/--warmup run stays within ~2.5 minutes
+    step_s = min(args.ref_step_seconds, 150.0 / max(1, args.steps + args.warmup))
+    cap = PER_GPU * max(1, args.gpus)
+    n = calibrate_sample(orc, inc_o, inc_m, 0, threads, step_s, cap)
     for w in range(args.warmup):
+        t = time.perf_counter()
         orc.search_round(inc_o, inc_m, SEED, MOVES["shift_permille"], MOVES["max_shift"], w, 0, n, threads)
+        # re-size the sample from the measured warm-up throughput
+        n = max(threads, min(cap, int(step_s * n / max(time.perf_counter() - t, 1e-3))))
     times = []
     for k in range(args.steps):
         t = time.perf_counter()
