@@ -192,6 +192,29 @@ class LocalSearch:
         return SearchResult(sched, self.makespan, self.initial_makespan, self.round, self.evaluated,
                             elapsed, list(self.improvements))
 
+    # -- checkpoint / resume: the search state is the incumbent, the round and the
+    # improvement trail; the base recording is rebuilt from the incumbent on load
+    def state_dict(self) -> dict:
+        return {"inc_orders": self.inc_orders.cpu().numpy().view(np.uint16).copy(),
+                "inc_mask": self.inc_mask.cpu().numpy().view(np.uint32).copy(),
+                "round": self.round, "makespan": self.makespan, "initial_makespan": self.initial_makespan,
+                "evaluated": self.evaluated, "config": dict(self.cfg.__dict__),
+                "improvements": [(i.round, i.makespan, i.timestamp, i.index) for i in self.improvements]}
+
+    def load_state_dict(self, state: dict) -> None:
+        import torch
+        if dict(state["config"]) != dict(self.cfg.__dict__):
+            raise ValueError("state was saved under another SearchConfig")
+        self.inc_orders.copy_(torch.from_numpy(np.asarray(state["inc_orders"], np.uint16).view(np.int16)))
+        self.inc_mask.copy_(torch.from_numpy(np.asarray(state["inc_mask"], np.uint32).view(np.int32)))
+        self.round = int(state["round"])
+        self.makespan = int(state["makespan"])
+        self.initial_makespan = int(state["initial_makespan"])
+        self.evaluated = int(state["evaluated"])
+        self.improvements = [Improvement(r, m, t, i) for r, m, t, i in state["improvements"]]
+        if self.base is not None:
+            self.base.record(self.inc_orders, self.inc_mask)
+
     def materialize(self, first: int, count: int, rnd: int | None = None):
         """Neighbours [first, first+count) of round `rnd` as full candidate tensors (for parity)."""
         import torch

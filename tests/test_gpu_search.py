@@ -1,5 +1,7 @@
 """GPU local search vs its CPU restatement (oracle/ps_oracle.c): moves, rounds, whole searches."""
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -296,3 +298,55 @@ def test_host_buffer_path_matches_device_path(cuda_ok):
         assert (host.flags == dev.flags.cpu().numpy()).all()
         assert (host.makespan == dev.makespan.cpu().numpy()).all()
         assert (host.peak == dev.peak.cpu().numpy()).all()
+
+
+def test_search_resumes_from_a_checkpoint(cuda_ok):
+    """state_dict / load_state_dict: a search stopped after 3 rounds and resumed in a new
+    LocalSearch follows the uninterrupted one exactly."""
+    inst, orders, off, LocalSearch, SearchConfig = _setup(2)
+    cfg = SearchConfig(seed=SEED, neighbours=2048, shift_permille=PERMILLE, max_shift=MAXSHIFT)
+    full = LocalSearch(inst, orders, off, cfg)
+    full.run(rounds=6)
+    part = LocalSearch(inst, orders, off, cfg)
+    part.run(rounds=3)
+    state = part.state_dict()
+    resumed = LocalSearch(inst, orders, off, cfg)
+    resumed.load_state_dict(state)
+    resumed.run(rounds=6)
+    assert resumed.makespan == full.makespan
+    assert [(i.round, i.makespan, i.index) for i in resumed.improvements] == \
+        [(i.round, i.makespan, i.index) for i in full.improvements]
+    assert (resumed.inc_orders.cpu() == full.inc_orders.cpu()).all()
+
+
+@pytest.mark.timeout(600)
+def test_kernels_are_memcheck_clean(cuda_ok):
+    """compute-sanitizer memcheck over a recording, a bounded search, a host-buffer batch and the
+    node bounds (sanitizers on the GPU box)."""
+    import os
+    import shutil
+    import subprocess
+    import sys
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not installed")
+    script = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch\n"
+        "from paper_2510_05186_b200 import workloads\n"
+        "from paper_2510_05186_b200.heuristics import best_feasible\n"
+        "from paper_2510_05186_b200.listsched import stage_order_of\n"
+        "from paper_2510_05186_b200.search import LocalSearch, SearchConfig\n"
+        "from paper_2510_05186_b200.bound import lower_bounds\n"
+        "inst = workloads.CONFIGS[2]()\n"
+        "s, _ = best_feasible(inst)\n"
+        "o = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}\n"
+        "ls = LocalSearch(inst, o, s.offloaded, SearchConfig(seed=1, neighbours=512))\n"
+        "ls.run(rounds=3)\n"
+        "od, md = ls.materialize(0, 256)\n"
+        "ls.di.evaluate_host(od.cpu().numpy().astype(np.uint8), md.cpu().numpy(), base=ls.base)\n"
+        "print(lower_bounds(inst, [(0, {i: 0 for i in range(1, inst.num_stages + 1)}, {})]))\n"
+    ) % str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "3", "--print-limit", "5",
+                        sys.executable, "-c", script], capture_output=True, text=True, timeout=540)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]

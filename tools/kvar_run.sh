@@ -1,1 +1,2 @@
-for n in 16384 32768 65536 131072; do KVAR_INCUMBENT=tools/inc320_config3.npz timeout 100 python tools/kvar.py 3 $n | cut -c60-200; done
+bash tools/ab.sh paper_2510_05186_b200/_lib/var/libps_prev.so paper_2510_05186_b200/_lib/libpipesched_b200.so 3 2
+KVAR_INCUMBENT=tools/inc320_config3.npz bash tools/ab.sh paper_2510_05186_b200/_lib/var/libps_prev.so paper_2510_05186_b200/_lib/libpipesched_b200.so 3
