@@ -39,6 +39,18 @@ def t(fn, reps=5):
 print("h2d 8-bit orders  ms", t(lambda: dev8.copy_(h8, non_blocking=True)), "bytes", h8.numel())
 print("eval device u8    ms", t(lambda: ls.di.evaluate(od8, md, peak=True, base=ls.base)))
 print("eval device u16   ms", t(lambda: ls.di.evaluate(od, md, peak=True, base=ls.base)))
+nb = ls.di.alloc_results(n, peak=True, blocked=False)
+print("eval device u8 no blocked ms", t(lambda: ls.di.evaluate(od8, md, base=ls.base, out=nb)))
+import ctypes as _C
+from paper_2510_05186_b200 import _native as _N
+bk = torch.empty(1, dtype=torch.int64, device="cuda")
+def _search():
+    bk.fill_(_N.BEST_NONE)
+    d = _N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), 0, 0, n, ls.moves, None, ls.base.handle)
+    ms = torch.empty(n, dtype=torch.int64, device="cuda")
+    _N.check(ls.lib.ps_search_round(ls.di.handle, _C.byref(d), _C.c_void_p(bk.data_ptr()), _C.c_void_p(ms.data_ptr()),
+                                    _C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+print("search round (same neighbours, makespans out) ms", t(_search))
 print("eval device nobase ms", t(lambda: ls.di.evaluate(od8, md, peak=True)))
 import numpy as np
 ho, hmm = h8.numpy(), hm.numpy()
