@@ -229,9 +229,17 @@ def main():
     from paper_2510_05186_b200.search import LocalSearch, SearchConfig
 
     rank, world, local = dist_env()
+    # PS_SHARE_GPU=1 (tests only): several ranks on one device over gloo, to exercise the sharded
+    # path where only one GPU is available; the product path is one rank per GPU over NCCL
+    share = os.environ.get("PS_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
 
