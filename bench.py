@@ -444,7 +444,9 @@ def main():
                "rounds_to_best": (last.round + 1) if last else 0,
                "seconds_to_best": last.timestamp if last else 0.0, "search_seconds": elapsed,
                "stopped_by": "16 rounds without improvement" if stale >= 16 else f"round cap {args.ttb_rounds}",
-               "neighbours_per_round": cfg.neighbours}
+               "neighbours_per_round": cfg.neighbours,
+               "note": "LocalSearch as shipped: a move drawn several times in a round is simulated once "
+                       "(lowest index); the trajectory is that of evaluating every neighbour"}
         if "cpu_baseline" in line:
             ttb["cpu_port_seconds_to_best_estimate"] = ttb["rounds_to_best"] * cfg.neighbours / line["cpu_baseline"]["value"]
         line["time_to_best"] = ttb

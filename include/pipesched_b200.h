@@ -134,6 +134,9 @@ typedef struct ps_search_desc {
     ps_move_params moves;
     int64_t *events_total;          /* device int64[2] (optional): as in ps_result_batch           */
     const ps_base *base;            /* optional: the incumbent recorded with ps_base_record        */
+    int32_t dedup;                  /* 1 (with a base, no makespan_out): a move drawn several times
+                                       in the round is simulated once, by its lowest index — the
+                                       round's best key is the same                              */
 } ps_search_desc;
 
 /* A batch of branch-and-bound nodes (device buffers): the state solver._Search._bound reads. */

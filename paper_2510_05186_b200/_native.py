@@ -111,6 +111,7 @@ class SearchDesc(C.Structure):
         ("moves", MoveParams),
         ("events_total", C.c_void_p),
         ("base", C.c_void_p),
+        ("dedup", C.c_int32),
     ]
 
 

@@ -1,6 +1,7 @@
 // ps_abi.cu — C ABI (include/pipesched_b200.h): instance tables, launch planning, search kernels.
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -440,8 +441,72 @@ __global__ void divergence_kernel(MoveCtx c, ps_move_params mp, uint64_t round, 
     idx[n] = (int32_t)n;
 }
 
+// Distinct moves of a round, in LPT order: key = divergence:15 | shift:1 | stage:5 | a:13 | b:13 |
+// index:17 (an adjacent shift a->a+1 is the same permutation as a+1->a; a no-op has a = b = 8191).
+__global__ void dedup_key_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first, int64_t count,
+                                 const uint32_t *cstep, const uint32_t *fstep, unsigned long long *key) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= count) return;
+    const Move mv = ctx_decode(c, mp, round, (uint64_t)(first + n));
+    uint32_t d = 0x7FFFu, sh = 0, st = 0, a = 8191, bb = 8191;
+    if (mv.type == MOVE_SHIFT) {
+        const int q = mv.a < mv.b ? mv.a : mv.b;
+        d = q == 0 ? 0u : cstep[mv.stage * c.L + q - 1];
+        sh = 1; st = mv.stage; a = mv.a; bb = mv.b;
+        if (mv.a - mv.b == 1 || mv.b - mv.a == 1) { a = q; bb = q + 1; }
+    } else if (mv.type == MOVE_TOGGLE) {
+        d = fstep[mv.stage * c.m + mv.mb];
+        st = mv.stage; a = mv.mb; bb = 0;
+    }
+    if (d > 0x7FFFu) d = 0x7FFFu;
+    key[n] = ((unsigned long long)d << 49) | ((unsigned long long)sh << 48) | ((unsigned long long)st << 43) |
+             ((unsigned long long)a << 30) | ((unsigned long long)bb << 17) | (unsigned long long)n;
+}
+
+__global__ void dedup_head_kernel(const unsigned long long *sorted, int64_t count, int32_t *idx, unsigned char *head) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= count) return;
+    idx[n] = (int32_t)(sorted[n] & 0x1FFFFull);
+    head[n] = n == 0 || (sorted[n] >> 17) != (sorted[n - 1] >> 17);
+}
+
 int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *order, cudaStream_t s) {
     const int64_t N = p.N;
+    ps_move_params mp;
+    mp.seed = p.seed;
+    mp.shift_permille = p.shift_permille;
+    mp.max_shift = p.max_shift;
+    if (p.dedup && N <= (1 << 17) && 3 * I->m < 8191 && 3 * I->P * I->m < 0x7FFF) {
+        // the same move drawn several times in a round is simulated once: its lowest index
+        // carries it, so the round's best key is unchanged
+        unsigned long long *keys = nullptr, *sorted = nullptr;
+        int32_t *idx = nullptr;
+        unsigned char *head = nullptr;
+        void *tmp = nullptr;
+        size_t b1 = 0, b2 = 0;
+        PS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, keys, sorted, (int)N, 0, 64, s));
+        PS_CUDA(cub::DeviceSelect::Flagged(nullptr, b2, idx, head, order + 1, order, (int)N, s));
+        PS_CUDA(cudaMallocAsync((void **)&keys, (size_t)N * 8, s));
+        PS_CUDA(cudaMallocAsync((void **)&sorted, (size_t)N * 8, s));
+        PS_CUDA(cudaMallocAsync((void **)&idx, (size_t)N * 4, s));
+        PS_CUDA(cudaMallocAsync((void **)&head, (size_t)N, s));
+        PS_CUDA(cudaMallocAsync(&tmp, std::max(b1, b2), s));
+        const unsigned g = (unsigned)((N + 255) / 256);
+        dedup_key_kernel<<<g, 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N, p.cstep, p.fstep, keys);
+        PS_CUDA(cudaGetLastError());
+        size_t tb = std::max(b1, b2);
+        PS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)N, 0, 64, s));
+        dedup_head_kernel<<<g, 256, 0, s>>>(sorted, N, idx, head);
+        PS_CUDA(cudaGetLastError());
+        tb = std::max(b1, b2);
+        PS_CUDA(cub::DeviceSelect::Flagged(tmp, tb, idx, head, order + 1, order, (int)N, s));
+        cudaFreeAsync(keys, s);
+        cudaFreeAsync(sorted, s);
+        cudaFreeAsync(idx, s);
+        cudaFreeAsync(head, s);
+        cudaFreeAsync(tmp, s);
+        return PS_OK;
+    }
     uint32_t *keys = nullptr, *keys_out = nullptr;
     int32_t *idx = nullptr;
     void *tmp = nullptr;
@@ -451,10 +516,6 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
     PS_CUDA(cudaMallocAsync((void **)&keys_out, (size_t)N * 4, s));
     PS_CUDA(cudaMallocAsync((void **)&idx, (size_t)N * 4, s));
     PS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
-    ps_move_params mp;
-    mp.seed = p.seed;
-    mp.shift_permille = p.shift_permille;
-    mp.max_shift = p.max_shift;
     divergence_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N,
                                                                  p.cstep, p.fstep, keys, idx, order);
     PS_CUDA(cudaGetLastError());
@@ -993,6 +1054,7 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.max_shift = d->moves.max_shift;
     p.makespan = makespan_out;
     p.best_key = (long long *)best_key;
+    p.dedup = makespan_out == nullptr && d->dedup;
     p.events_total = (unsigned long long *)d->events_total;
     return run_eval(I, p, true, (cudaStream_t)stream, d->base);
 }

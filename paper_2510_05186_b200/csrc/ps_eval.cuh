@@ -76,6 +76,7 @@ struct EvalParams {
     // is non-zero; the copy engine writes each flag after its chunk's data, on the same stream
     const int32_t *ready;
     long long ready_chunk;
+    int dedup;               // (host side) evaluate each distinct move of a round once
     const int32_t *work_list;
     const int32_t *work_count;
     // per-candidate state

@@ -36,6 +36,7 @@ class SearchConfig:
     shift_permille: int = 700        # SHIFT moves; the rest toggle offload bits
     max_shift: int = 4
     share_prefix: bool = True        # resume neighbours from checkpoints of the incumbent
+    dedup: bool = True               # simulate a move drawn several times in a round once
 
 
 @dataclass
@@ -132,7 +133,7 @@ class LocalSearch:
         self.best_key.fill_(N.BEST_NONE)
         desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round,
                             self.first, self.count, self.moves, None,
-                            self.base.handle if self.base is not None else None)
+                            self.base.handle if self.base is not None else None, int(self.cfg.dedup))
         N.check(self.lib.ps_search_round(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
                                          C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None,
                                          self._stream()))
