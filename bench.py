@@ -155,6 +155,51 @@ def calibrate_sample(orc, inc_o, inc_m, rnd, threads, target_s, cap):
     return max(threads, min(cap, n))
 
 
+def _philox_np(c0, c1, c2, c3, k0, k1):
+    """Philox4x32-10 over numpy arrays (the move decode of DESIGN.md §4, host-side analysis only)."""
+    import numpy as np
+    M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+    c0, c1, c2, c3 = [np.asarray(x, np.uint32) for x in (c0, c1, c2, c3)]
+    for r in range(10):
+        if r:
+            k0 = (k0 + 0x9E3779B9) & 0xFFFFFFFF
+            k1 = (k1 + 0xBB67AE85) & 0xFFFFFFFF
+        p0 = M0 * c0.astype(np.uint64)
+        p1 = M1 * c2.astype(np.uint64)
+        c0, c1, c2, c3 = ((p1 >> np.uint64(32)).astype(np.uint32) ^ c1 ^ np.uint32(k0), p1.astype(np.uint32),
+                          (p0 >> np.uint64(32)).astype(np.uint32) ^ c3 ^ np.uint32(k1), p0.astype(np.uint32))
+    return c0, c1, c2, c3
+
+
+def distinct_move_fraction(inst, rounds, neighbours):
+    """Share of a round's neighbours that are distinct moves (adjacent shifts a<->a+1 coincide;
+    no-ops coincide), averaged over `rounds` — what a deduplicating CPU search would simulate."""
+    import numpy as np
+    from paper_2510_05186_b200 import OpId, OpKind
+    P, m, L = inst.num_stages, inst.num_microbatches, 3 * inst.num_microbatches
+    offl = np.array([[inst.act_size.get(OpId(s + 1, j + 1, OpKind.F), 0) > 0 for j in range(m)]
+                     for s in range(P)])
+    any_off = bool(offl.any())
+    idx = np.arange(neighbours, dtype=np.uint64)
+    fr = []
+    for rnd in rounds:
+        r0, r1, r2, r3 = _philox_np(idx.astype(np.uint32), (idx >> np.uint64(32)).astype(np.uint32),
+                                    np.full(neighbours, rnd & 0xFFFFFFFF, np.uint32),
+                                    np.full(neighbours, rnd >> 32, np.uint32), SEED & 0xFFFFFFFF, SEED >> 32)
+        st = (r1 % P).astype(np.int64)
+        shift = (~np.bool_(any_off)) | ((r0 % 1000) < MOVES["shift_permille"])
+        a = (r2 % L).astype(np.int64)
+        d = 1 + ((r3 >> 1) % MOVES["max_shift"]).astype(np.int64)
+        b = np.clip(np.where(r3 & 1, a - d, a + d), 0, L - 1)
+        j = (r2 % m).astype(np.int64)
+        lo, hi = np.minimum(a, b), np.maximum(a, b)
+        adj = (hi - lo) == 1
+        key = np.where(shift, np.where(b == a, -1, (st * 8192 + np.where(adj, lo, a)) * 8192 + np.where(adj, hi, b)),
+                       np.where(offl[st, j], -2 - (st * m + j), -1))
+        fr.append(len(np.unique(key)) / neighbours)
+    return float(np.mean(fr))
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm's CPU restatement (oracle port), all host threads."""
     rank, world, _ = dist_env()
@@ -449,6 +494,10 @@ def main():
                        "(lowest index); the trajectory is that of evaluating every neighbour"}
         if "cpu_baseline" in line:
             ttb["cpu_port_seconds_to_best_estimate"] = ttb["rounds_to_best"] * cfg.neighbours / line["cpu_baseline"]["value"]
+            # the same search on the CPU with the same deduplication of repeated moves
+            frac = distinct_move_fraction(inst, range(4), cfg.neighbours)
+            ttb["distinct_move_fraction"] = frac
+            ttb["cpu_port_seconds_to_best_estimate_dedup"] = ttb["cpu_port_seconds_to_best_estimate"] * frac
         line["time_to_best"] = ttb
     line["search"] = {"initial_makespan": ls.initial_makespan, "final_makespan": ls.makespan,
                       "warm_start": gen_name, "rounds": ls.round,
