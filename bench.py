@@ -374,6 +374,12 @@ def main():
         except Exception:
             traffic = None
     n_cand = cfg.neighbours // world
+    hbm_peak, hbm_src = 7700.0, "B200_PROFILING.md nominal (MEASURED_PEAKS.json absent)"
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+    except Exception:
+        pass
     line["roofline"] = {
         "bound": "int32-issue", "achieved": achieved, "peak": int32_peak, "unit": "Tops/s",
         "frac": achieved / int32_peak, "traffic": traffic,
@@ -384,7 +390,8 @@ def main():
         "peak_source": "ps_int32_probe measured live on this GPU (IADD3/LOP3/IMAD chains)",
         "hbm": {"algorithmic_bytes_per_launch": n_cand * (16 + 20 + 8 * inst.num_stages),
                 "achieved_gbs": n_cand * (16 + 20 + 8 * inst.num_stages) / kern_s / 1e9,
-                "peak_gbs": 6536.0, "note": "not the binding roof: move-encoded candidates"},
+                "peak_gbs": hbm_peak, "peak_gbs_source": hbm_src,
+                "note": "not the binding roof: move-encoded candidates"},
         "note": "latency-bound discrete-event simulation (SURVEY.md 8(d)): achieved counts the algorithmic "
                 "work of every evaluated candidate (10 int ops x its 3Pm + 2|off| events); prefix and suffix "
                 "sharing simulate only simulated_events_per_launch of them"}
