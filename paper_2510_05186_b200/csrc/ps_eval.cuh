@@ -565,6 +565,25 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                  (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
                  (long long)top == *reinterpret_cast<const long long *>(rg + 14);
         }
+#ifdef PS_DEBUG_CONV
+        // diagnostics build: histogram of the first failing component into events_total[2 + r]
+        auto dbg = [&](int r) { if (lane == 0 && p.events_total) atomicAdd(p.events_total + 2 + r, 1ull); };
+        {
+            int r = 99;
+            if (has_stage) {
+                if (pos != (int)rg[0]) r = 0;
+                else if (sfree - (int)rg[1] != d) r = 1;
+                else if (!(cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u))) r = 2;
+                else if (we - ws != (int)rg[4]) r = 3;
+                else if (n_poff != (int)rg[5] || n_prel != (int)rg[6] || n_unrel != (int)rg[7]) r = 4;
+                else if ((first_start == INT_MAX) != ((int)rg[8] == INT_MAX)) r = 5;
+                else if ((long long)base != *reinterpret_cast<const long long *>(rg + 12) ||
+                         (long long)top != *reinterpret_cast<const long long *>(rg + 14)) r = 6;
+            }
+            r = __reduce_min_sync(0xffffffffu, r);
+            if (r != 99) dbg(r);
+        }
+#endif
         if (!__all_sync(0xffffffffu, eq)) return false;
         // end-time words (time << 2 | state): a time the base's checkpoint still carries (it
         // matters there) must be the candidate's moved by delta; a time the checkpoint dropped must
@@ -584,8 +603,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             }
             eq = eq && ok;
         }
+#ifdef PS_DEBUG_CONV
+        if (!__all_sync(0xffffffffu, eq)) { dbg(7); return false; }
+#endif
         for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
             eq = eq && SW(o_A + (k)) == src[k];
+#ifdef PS_DEBUG_CONV
+        if (!__all_sync(0xffffffffu, eq)) { dbg(8); return false; }
+#endif
         if (has_stage && eq) {
             const uint32_t *st = src + ck_t + i * p.ck_kc;
             const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
@@ -593,6 +618,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 eq = (int)SW(o_wt + (ws + q)) - (int)st[q] == d && SV(o_wu + (ws + q)) == su[q];
         }
         conv_delta = d;
+#ifdef PS_DEBUG_CONV
+        if (!__all_sync(0xffffffffu, eq)) dbg(9); else dbg(11);
+#endif
         return __all_sync(0xffffffffu, eq);
     };
 

@@ -19,9 +19,9 @@ orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
 n = 8192
 ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=n, shift_permille=700, max_shift=4))
 o, mk = ls.materialize(0, n, 0)
-r = ls.di.evaluate(o, mk, peak=False, base=ls.base)
+r = ls.di.evaluate(o, mk, base=ls.base, out=ls.di.alloc_results(n, peak=False, blocked=False))
 torch.cuda.synchronize()
-bl = r.blocked.cpu().numpy().astype(np.uint32)
+bl = r.bubble.cpu().numpy().astype(np.uint32)
 ev, e0 = bl & 0xFFFF, bl >> 16
 fl = r.flags.cpu().numpy()
 orc = Oracle(ls.di.packed)
