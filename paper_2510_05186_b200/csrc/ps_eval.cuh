@@ -175,6 +175,8 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     const int row_bytes = P * p.stride * (p.order_u8 ? 1 : 2);
 
     const int chan_i = has_stage ? __ldg(&p.chan[i]) : -1;
+    // this stage's host link is its own (no other stage transfers on it)
+    const bool chan_excl = __popc(__match_any_sync(0xffffffffu, chan_i)) == 1;
     const V limit_i = has_stage ? ldv<V>(p.limit, i) : V(0);
     const int rowbase = UNI ? is : is * m;
     // per-stage constants of microbatch-symmetric instances live in registers
@@ -287,7 +289,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     // below sfree, and below the channel's free time while this stage still has a transfer to come,
     // so no future query or insertion (this one included) lands under it.
     auto win_insert = [&](int t, V d) {
-        win_fold(n_unrel > 0 ? min(sfree, cfree) : sfree);
+        // (greedy channels: with no transfer of this stage in flight, every later transfer of it
+        // follows an F not committed yet, so nothing can land below the stage free time)
+        win_fold((derived ? (n_poff > 0 || n_prel > 0) : n_unrel > 0) ? min(sfree, cfree) : sfree);
         top += d;
         rF = rG = NO_R;                                // the ledger changed: drop cached answers
         int k = we - 1;
@@ -558,8 +562,12 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         // the per-stage scalars first: they tell a still-perturbed candidate apart cheaply
         if (has_stage) {
             // a channel that has carried nothing yet (free time 0 on both) constrains nothing
+            // (nor does an own channel with nothing in flight that is already behind the stage: every
+            // later transfer on it waits for an F not committed yet)
             eq = pos == (int)rg[0] && sfree - (int)rg[1] == d &&
-                 (cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u)) && we - ws == (int)rg[4] &&
+                 (cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u) ||
+                  (derived && chan_excl && n_poff == 0 && n_prel == 0 && cfree <= sfree && rg[2] <= rg[1])) &&
+                 we - ws == (int)rg[4] &&
                  n_poff == (int)rg[5] && n_prel == (int)rg[6] && n_unrel == (int)rg[7] &&
                  (first_start == INT_MAX) == ((int)rg[8] == INT_MAX) &&
                  (long long)base == *reinterpret_cast<const long long *>(rg + 12) &&
@@ -582,6 +590,16 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             }
             r = __reduce_min_sync(0xffffffffu, r);
             if (r != 99) dbg(r);
+            // would exempting finished stages (pos == L in both) from the time/window checks pass?
+            int r2 = 99;
+            if (has_stage && !(pos == L && (int)rg[0] == L)) {
+                if (pos != (int)rg[0]) r2 = 0;
+                else if (sfree - (int)rg[1] != d) r2 = 1;
+                else if (!(cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u))) r2 = 2;
+                else if (we - ws != (int)rg[4]) r2 = 3;
+            }
+            r2 = __reduce_min_sync(0xffffffffu, r2);
+            if (r != 99 && r2 == 99) dbg(10);
         }
 #endif
         if (!__all_sync(0xffffffffu, eq)) return false;

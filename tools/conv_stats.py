@@ -22,7 +22,7 @@ N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(ls.best_k
                                C.c_void_p(torch.cuda.current_stream().cuda_stream)))
 torch.cuda.synchronize()
 names = ["pos", "sfree shift", "cfree", "window count", "pending counts", "first_start", "base/top",
-         "end-time words", "pending bitsets", "window contents", "-", "converged"]
+         "end-time words", "pending bitsets", "window contents", "ok if finished stages exempt", "converged"]
 v = ev.cpu().tolist()
 print("simulated", v[0], "algorithmic", v[1])
 for k, nm in enumerate(names):
