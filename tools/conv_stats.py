@@ -15,6 +15,12 @@ s0, _ = best_feasible(inst)
 orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
 n = 65536
 ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=n, shift_permille=700, max_shift=4))
+if os.environ.get("KVAR_INCUMBENT"):
+    import numpy as np
+    z = np.load(os.environ["KVAR_INCUMBENT"])
+    ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
+    ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
+    ls.base.record(ls.inc_orders, ls.inc_mask)
 ev = torch.zeros(16, dtype=torch.int64, device="cuda")
 ls.best_key.fill_(N.BEST_NONE)
 desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), 0, 0, n, ls.moves, ev.data_ptr(), ls.base.handle)
