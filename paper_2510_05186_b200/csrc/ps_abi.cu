@@ -40,7 +40,11 @@ struct ps_instance {
 struct ps_base {
     const ps_instance *inst;
     int K, cand_words, ck_words, ck_interval, ck_max;
-    int max_window;     // widest live ledger window the base needed (-1: unknown / unusable)
+    mutable int max_window;     // widest live ledger window the base needed (-1: unknown / unusable)
+    // the recording's info reaches the host asynchronously (no stream sync per recording)
+    int32_t *h_info = nullptr;  // pinned [8]
+    cudaEvent_t info_ev = nullptr;
+    mutable bool info_pending = false;
     uint32_t *ck;       // [ck_max][ck_words]
     uint32_t *cstep;    // [P][L]
     uint32_t *fstep;    // [P][m]
@@ -246,12 +250,22 @@ void attach_base(const ps_base *B, EvalParams *p) {
 // reads its worklist from device memory: no host round trip.
 int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *order, cudaStream_t s);
 
+// Pick up the last recording's info (its copy was queued behind the recording; by the time a
+// round needs it, it has long landed).
+void refresh_info(const ps_base *B) {
+    if (!B->info_pending) return;
+    cudaEventSynchronize(B->info_ev);
+    B->max_window = B->h_info[0] > 0 ? B->h_info[4] : -1;
+    B->info_pending = false;
+}
+
 int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr) {
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
     const int full = 5 * I->m;
     int K1 = window_size(I);
     // with a recorded base, neighbours need about the base's window: size the first pass from it
+    if (B) refresh_info(B);
     if (B && B->inst == I && B->max_window >= 0 && !getenv("PS_WINDOW"))
         K1 = std::min(full, std::max(8, B->max_window + 4));
     int Ks[3] = {K1, std::min(full, 4 * K1), full};
@@ -735,6 +749,8 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_orders, (size_t)I->P * I->stride * 2);
     if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_mask, (size_t)I->mask_words * 4);
     if (e == cudaSuccess) e = cudaMemset(B->info, 0xFF, 8 * sizeof(int32_t));   // -1: nothing recorded
+    if (e == cudaSuccess) e = cudaHostAlloc((void **)&B->h_info, 8 * sizeof(int32_t), cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&B->info_ev, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         ps_base_destroy(B);
         return fail(PS_ERR_NOMEM, "base workspace: %s", cudaGetErrorString(e));
@@ -755,6 +771,9 @@ int ps_base_destroy(ps_base *B) {
     cudaFree(B->mask);
     cudaFree(B->prev_orders);
     cudaFree(B->prev_mask);
+    if (B->info_pending) cudaEventSynchronize(B->info_ev);
+    if (B->h_info) cudaFreeHost(B->h_info);
+    if (B->info_ev) cudaEventDestroy(B->info_ev);
     delete B;
     return PS_OK;
 }
@@ -767,6 +786,7 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     cudaStream_t s = (cudaStream_t)stream;
     // A usable previous recording is kept: the new base replays it up to their first difference
     // (its checkpoints, cstep and fstep entries before that point are the new base's too).
+    refresh_info(B);
     const bool resume = B->max_window >= 0 && env_int("PS_REC_RESUME", 1) != 0;
     if (resume) {
         PS_CUDA(cudaMemcpyAsync(B->prev_orders, B->orders, (size_t)I->P * I->stride * 2, cudaMemcpyDeviceToDevice, s));
@@ -817,10 +837,9 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
         PS_CUDA(cudaGetLastError());
     }
     // the evaluation passes size their ledger window from the base's (one host read per record)
-    int32_t info[8];
-    PS_CUDA(cudaMemcpyAsync(info, B->info, sizeof info, cudaMemcpyDeviceToHost, s));
-    PS_CUDA(cudaStreamSynchronize(s));
-    B->max_window = info[0] > 0 ? info[4] : -1;
+    PS_CUDA(cudaMemcpyAsync(B->h_info, B->info, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    PS_CUDA(cudaEventRecord(B->info_ev, s));
+    B->info_pending = true;
     return PS_OK;
 }
 
