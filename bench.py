@@ -230,7 +230,7 @@ def run_reference(args):
         times.append(time.perf_counter() - t)
     total = sum(times)
     value = n * args.steps / total
-    sample = f"first {n} neighbours of each round (of {PER_GPU * max(1, args.gpus)}), config 3 AdaOffload incumbent"
+    sample = f"first {n} neighbours of each round (of {PER_GPU * max(1, args.gpus)}), config {CONFIG} warm-start incumbent"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
@@ -241,9 +241,11 @@ def run_reference(args):
 
 
 def workload_config(world):
-    return {"workload": "config3: Llama-7B synthetic 8 stages x 64 microbatches, PCIe-limited offload, "
-                        "AdaOffload incumbent, 65536 neighbours/round/GPU",
-            "stages": 8, "microbatches": 64, "candidates_per_round": PER_GPU * world,
+    from paper_2510_05186_b200 import workloads
+    inst = workloads.CONFIGS[CONFIG]()
+    doc = " ".join((workloads.CONFIGS[CONFIG].__doc__ or "").split())
+    return {"workload": f"config{CONFIG}: {doc} AdaOffload/best_feasible incumbent, {PER_GPU} neighbours/round/GPU",
+            "stages": inst.num_stages, "microbatches": inst.num_microbatches, "candidates_per_round": PER_GPU * world,
             "candidates_per_gpu": PER_GPU, "parallelism": f"candidates sharded over {world} GPU(s)",
             "l2": "flushed (256 MiB write) between timed steps",
             "moves": MOVES, "seed": SEED}
@@ -261,7 +263,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttb", action="store_true")
     ap.add_argument("--ttb-rounds", type=int, default=1000)
+    # other BASELINE configs for manual runs (the driver's line is config 3, 65,536 per GPU)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--per-gpu", type=int, default=65536)
     args = ap.parse_args()
+    global CONFIG, PER_GPU
+    CONFIG, PER_GPU = args.config, args.per_gpu
     if args.impl == "reference":
         return run_reference(args)
 
