@@ -164,6 +164,7 @@ int window_size(const ps_instance *I) { return std::min(std::max(4, env_int("PS_
 // in shared memory; the state moves to global memory only when a single warp's does not fit.
 // `N` bounds the grid (a worklist pass may receive fewer candidates, never more).
 int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int order_bytes = 2) {
+    K = (K + 1) & ~1;            // even: the state words after the windows start on a 16-byte boundary
     pl->K = K;
     pl->cand_words = words_per_candidate(I, K, moves ? 0 : order_bytes);
     pl->inc_words = incumbent_words(I, moves);
@@ -726,7 +727,8 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
     ps_base *B = new (std::nothrow) ps_base();
     if (!B) return fail(PS_ERR_NOMEM, "host allocation");
     B->inst = I;
-    B->K = std::min(5 * I->m, 128);                 // recording window (checkpoints store it compactly)
+    B->K = (std::min(5 * I->m, 128) + 1) & ~1;     // recording window (checkpoints store it compactly);
+                                                    // even, like a pass's (16-byte aligned state words)
     B->max_window = -1;
     B->cand_words = words_per_candidate(I, B->K, 2);
     {
@@ -734,7 +736,7 @@ int ps_base_create(const ps_instance *I, ps_base **out) {
         const int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
         const int ck_t = (nz + 1) & ~1;
         const int ck_u = (ck_t + I->P * B->K + 1) & ~1;
-        B->ck_words = ck_u + I->P * B->K * vw + 32 * CK_REGW;
+        B->ck_words = (ck_u + I->P * B->K * vw + 32 * CK_REGW + 3) & ~3;   // 16-byte aligned checkpoints
     }
     // checkpoints every ck_interval compute events (3Pm per candidate)
     B->ck_interval = std::max(1, next_pow2(std::max(1, env_int("PS_CHECKPOINT_INTERVAL", 8))));

@@ -112,6 +112,26 @@ __device__ __forceinline__ V ldv(const void *base, int idx) {
 }
 
 // A candidate key: start in the high word, (rank, stage, microbatch, kind) in the low word.
+// A warp's state words in 16-byte vectors: `dst`/`src` are 16-byte aligned (the host keeps the
+// state block and every checkpoint on 4-word boundaries), the lanes stride over the vectors and
+// the few words past the last whole vector.  Rolled: these run once per candidate, and the unrolled
+// copies cost more in instruction fetch than they save.
+__device__ __forceinline__ void warp_zero_words(uint32_t *dst, int n, int lane) {
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    const int n4 = n >> 2;
+#pragma unroll 1
+    for (int k = lane; k < n4; k += 32) d4[k] = make_uint4(0u, 0u, 0u, 0u);
+    for (int k = (n4 << 2) + lane; k < n; k += 32) dst[k] = 0u;
+}
+__device__ __forceinline__ void warp_copy_words(uint32_t *dst, const uint32_t *src, int n, int lane) {
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    const int n4 = n >> 2;
+#pragma unroll 1
+    for (int k = lane; k < n4; k += 32) d4[k] = s4[k];
+    for (int k = (n4 << 2) + lane; k < n; k += 32) dst[k] = src[k];
+}
+
 __device__ __forceinline__ unsigned long long make_key(uint32_t hi, uint32_t lo) {
     return ((unsigned long long)hi << 32) | lo;
 }
@@ -122,6 +142,30 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 // the global-state variant keeps its registers.
 #ifndef PS_MIN_BLOCKS
 #define PS_MIN_BLOCKS 7
+#endif
+// Data-dependent loops over ledger-window slots and state words stay rolled where the A/B says so:
+// unrolled copies pushed the kernel past the instruction cache (ncu: no_instruction stalls 27%
+// move-encoded, 45% materialised) and cost more in fetch than they saved in issue (r01 A/B,
+// DESIGN.md §3.10).  PS_ROLL_HOT: event-loop window loops rolled 0 nowhere, 1 everywhere, 2 in the
+// materialised-candidate kernels only (default: the move-encoded kernel gains from its unrolled
+// copies on every config but the first rounds of config 3); PS_ROLL_COLD: the once-per-candidate ones.
+#ifndef PS_ROLL_HOT
+#define PS_ROLL_HOT 2
+#endif
+#ifndef PS_ROLL_COLD
+#define PS_ROLL_COLD 1
+#endif
+#if PS_ROLL_HOT == 1
+#define PS_HOT_LOOP(...) _Pragma("unroll 1") __VA_ARGS__
+#elif PS_ROLL_HOT == 2          // rolled in the materialised-candidate kernels only
+#define PS_HOT_LOOP(...) if constexpr (MOVES) { __VA_ARGS__ } else { _Pragma("unroll 1") __VA_ARGS__ }
+#else
+#define PS_HOT_LOOP(...) __VA_ARGS__
+#endif
+#if PS_ROLL_COLD
+#define PS_NOUNROLL_C _Pragma("unroll 1")
+#else
+#define PS_NOUNROLL_C
 #endif
 #ifndef PS_TAU_PAIR
 #define PS_TAU_PAIR 0   // measured slower on B200 (r01): register pressure outweighs the saved scan
@@ -275,14 +319,14 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     // holding the usage AFTER it; slots [ws, we) of a 2K array, compacted when the end is reached.
     // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
     auto win_fold = [&](int line) {
-        while (ws < we && wlo < line) {
+        PS_HOT_LOOP(while (ws < we && wlo < line) {
             V u = SV(o_wu + (ws));
             peak = u > peak ? u : peak;
             if (REC) segpk = u > segpk ? u : segpk;
             base = u;
             ++ws;
             wlo = ws < we ? (int)SW(o_wt + (ws)) : INT_MAX;
-        }
+        })
         if (ws == we) whi = INT_MIN;
     };
     // Called before sfree / cfree / n_unrel reflect the event being committed: the fold line is
@@ -300,20 +344,20 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             return;
         }
         if (ws < we && t < whi) {
-            while (k >= ws && (int)SW(o_wt + (k)) > t) --k;     // last breakpoint at or before t
+            PS_HOT_LOOP(while (k >= ws && (int)SW(o_wt + (k)) > t) --k;)  // last breakpoint at or before t
             if (k >= ws && (int)SW(o_wt + (k)) == t) {          // same time: merge into that breakpoint
-                for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;
+                PS_HOT_LOOP(for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;)
                 return;
             }
         }
         if (we - ws == K) { ovf = true; return; }
         if (we == 2 * K) {                             // compact to the front
-            for (int q = ws; q < we; ++q) { SW(o_wt + (q - ws)) = SW(o_wt + (q)); SV(o_wu + (q - ws)) = SV(o_wu + (q)); }
+            PS_HOT_LOOP(for (int q = ws; q < we; ++q) { SW(o_wt + (q - ws)) = SW(o_wt + (q)); SV(o_wu + (q - ws)) = SV(o_wu + (q)); })
             k -= ws;
             we -= ws;
             ws = 0;
         }
-        for (int q = we - 1; q > k; --q) { SW(o_wt + (q + 1)) = SW(o_wt + (q)); SV(o_wu + (q + 1)) = SV(o_wu + (q)) + d; }
+        PS_HOT_LOOP(for (int q = we - 1; q > k; --q) { SW(o_wt + (q + 1)) = SW(o_wt + (q)); SV(o_wu + (q + 1)) = SV(o_wu + (q)) + d; })
         SW(o_wt + (k + 1)) = (uint32_t)t;
         SV(o_wu + (k + 1)) = (k >= ws ? SV(o_wu + (k)) : base) + d;
         ++we;
@@ -324,7 +368,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto win_tau = [&](V R) -> int {
         if (R < 0 || top > R) return TAU_NONE;
         int k = we - 1;
-        while (k >= ws && !(SV(o_wu + (k)) > R)) --k;
+        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > R)) --k;)
         if (k >= ws) return (int)SW(o_wt + (k + 1));
         return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
     };
@@ -333,9 +377,9 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
     auto tau_pair = [&]() {
         const V RF = limit_i - v0, RG = limit_i - v3;
         int k = we - 1;
-        while (k >= ws && !(SV(o_wu + (k)) > RF)) --k;
+        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > RF)) --k;)
         const int kF = k;
-        while (k >= ws && !(SV(o_wu + (k)) > RG)) --k;
+        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > RG)) --k;)
         auto conv = [&](V R, int kk) -> int {
             if (R < 0 || top > R) return TAU_NONE;
             if (kk >= ws) return (int)SW(o_wt + (kk + 1));
@@ -624,7 +668,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
 #ifdef PS_DEBUG_CONV
         if (!__all_sync(0xffffffffu, eq)) { dbg(7); return false; }
 #endif
-        for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
+        PS_NOUNROLL_C for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
             eq = eq && SW(o_A + (k)) == src[k];
 #ifdef PS_DEBUG_CONV
         if (!__all_sync(0xffffffffu, eq)) { dbg(8); return false; }
@@ -632,7 +676,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
         if (has_stage && eq) {
             const uint32_t *st = src + ck_t + i * p.ck_kc;
             const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
-            for (int q = 0; q < we - ws && eq; ++q)
+            PS_NOUNROLL_C for (int q = 0; q < we - ws && eq; ++q)
                 eq = (int)SW(o_wt + (ws + q)) - (int)st[q] == d && SV(o_wu + (ws + q)) == su[q];
         }
         conv_delta = d;
@@ -668,7 +712,7 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
             __syncwarp();
         }
         // ================= initialise ======================================================
-        for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = 0u;
+        warp_zero_words(&SW(o_A), nz, lane);
         if (!MOVES) {
             // stage the candidate's rows: 8-byte loads, coalesced across the warp
             const uint2 *src = reinterpret_cast<const uint2 *>(reinterpret_cast<const unsigned char *>(p.orders) +
@@ -849,11 +893,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 __syncwarp();
                 continue;
             }
-            for (int k = lane; k < nz; k += 32) SW(o_A + (k)) = src[k];
+            warp_copy_words(&SW(o_A), src, nz, lane);
             if (has_stage) {
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
-                for (int q = 0; q < we; ++q) { SW(o_wt + (q)) = st[q]; SV(o_wu + (q)) = su[q]; }
+                PS_NOUNROLL_C for (int q = 0; q < we; ++q) { SW(o_wt + (q)) = st[q]; SV(o_wu + (q)) = su[q]; }
                 wlo = we > 0 ? (int)st[0] : INT_MAX;
                 whi = we > 0 ? (int)st[we - 1] : INT_MIN;
             }
@@ -945,11 +989,11 @@ __global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval
                 if (REC && !(cc == cc0 && cc0 > 0)) {
                     if (c < p.ck_max) {
                         uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                        for (int q = lane; q < nz; q += 32) dst[q] = SW(o_A + (q));
+                        warp_copy_words(dst, &SW(o_A), nz, lane);
                         if (has_stage) {
                             uint32_t *st = dst + ck_t + i * p.ck_kc;
                             V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
-                            for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
+                            PS_NOUNROLL_C for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
                         }
                         const int ws0 = ws, we0 = we;
                         we -= ws;

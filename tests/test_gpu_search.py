@@ -214,10 +214,10 @@ def test_rerecorded_base_is_exact(cuda_ok, cfg):
         _eval_both(ls.di, o, mk, rb)
 
 
-def _base_tables(base, P, m, MW):
+def _base_tables(base, P, m, MW, vw=1):
     """A recorded base's tables with only what readers use: checkpoints up to the count, each
     with its state words, the live window slots and every lane's saved scalars (all but word 9,
-    the widest window so far, a sizing hint)."""
+    the widest window so far, a sizing hint).  `vw`: 32-bit words per ledger usage value."""
     from paper_2510_05186_b200 import _native as N
     info = np.frombuffer(base.read(N.BASE_INFO), np.int32).copy()
     res = np.frombuffer(base.read(N.BASE_RESULT), np.int64).copy()
@@ -229,9 +229,13 @@ def _base_tables(base, P, m, MW):
     cks = []
     for c in range(max(info[0], 0)):
         w = raw[c * ckw:(c + 1) * ckw]
-        regs = w[ck_r:ck_r + regw * P].reshape(P, regw)
+        regs = w[ck_r:ck_r + regw * P].reshape(P, regw).copy()
+        # an idle exclusive link's free time at or below the stage's is dead (the same_state
+        # relaxation): a re-recording that converged under it keeps its predecessor's shifted value
+        dead = (regs[:, 5] == 0) & (regs[:, 6] == 0) & (regs[:, 2] <= regs[:, 1])
+        regs[dead, 2] = 0xFFFFFFFF
         win = [(w[ck_t + s * kc: ck_t + s * kc + regs[s, 4]].tolist(),
-                w[ck_u + s * kc: ck_u + s * kc + regs[s, 4]].tolist()) for s in range(P)]
+                w[ck_u + vw * s * kc: ck_u + vw * (s * kc + regs[s, 4])].tolist()) for s in range(P)]
         # word 20 (the event step) is warp-wide: every lane's copy, not just the stage lanes'
         steps = w[ck_r:ck_r + regw * 32].reshape(32, regw)[:, 20].tolist()
         cks.append((w[:nz].tolist(), regs[:, list(range(9)) + list(range(10, 21))].tolist(), win, steps))
