@@ -51,6 +51,16 @@ summary = {
     "shared_load_instructions": num("smsp__sass_inst_executed_op_shared_ld.sum"),
     "sm_clock_ghz": num("smsp__cycles_elapsed.avg.per_second"),
 }
+stalls = {}
+for i, name in enumerate(h):
+    if name.startswith("smsp__pcsamp_warps_issue_stalled_") and not name.endswith("_not_issued"):
+        try:
+            stalls[name[len("smsp__pcsamp_warps_issue_stalled_"):]] = float(v[i].replace(",", ""))
+        except ValueError:
+            pass
+tot_s = sum(stalls.values()) or 1.0
+summary["stall_samples_pct"] = {k: round(100 * x / tot_s, 1) for k, x in
+                                sorted(stalls.items(), key=lambda kv: -kv[1]) if x / tot_s >= 0.005}
 summary["dram_bytes_per_launch"] = (summary["dram_bytes_read"] or 0) + (summary["dram_bytes_write"] or 0)
 lrows = [r for r in csv.reader(open(launches)) if len(r) > 10]
 lh = lrows[0]
