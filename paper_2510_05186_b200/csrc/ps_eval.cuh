@@ -167,13 +167,16 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #else
 #define PS_NOUNROLL_C
 #endif
+#ifndef PS_MIN_BLOCKS_MAT
+#define PS_MIN_BLOCKS_MAT 5   // materialised candidates: 102-register cap (r01 A/B)
+#endif
 #ifndef PS_TAU_PAIR
 #define PS_TAU_PAIR 0   // measured slower on B200 (r01): register pressure outweighs the saved scan
 #endif
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
 template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : PS_MIN_BLOCKS) eval_kernel(const EvalParams p) {
+__global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
