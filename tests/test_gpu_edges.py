@@ -1,0 +1,124 @@
+"""Edge cases of the batch API on the GPU: empty batches, malformed candidates (with and without a
+recorded base, in the register seen-set path m <= 64 and the shared-memory one m > 64), and the
+drop-in's error behaviour.  Every flag is compared with the C oracle's."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(cfg):
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.engine import DeviceInstance
+    from paper_2510_05186_b200.heuristics import generator_structures
+    from paper_2510_05186_b200.packing import encode_candidate, pack_instance
+    inst = workloads.CONFIGS[cfg]()
+    pk = pack_instance(inst)
+    base = [encode_candidate(pk, o, f) for o, f in generator_structures(inst)]
+    return inst, pk, base, DeviceInstance(inst, packed=pk)
+
+
+def _malformed_batch(pk, base, rng):
+    """Well-formed neighbours interleaved with every kind of structural damage."""
+    P, m = pk.num_stages, pk.num_microbatches
+    offl = np.argwhere(pk.act_size > 0)
+    not_offl = np.argwhere(pk.act_size <= 0)
+    rows, masks, kinds = [], [], []
+    for c in range(48):
+        o, mk, _ = base[c % len(base)]
+        o, mk = o.copy(), mk.copy()
+        i = int(rng.integers(P))
+        a = int(rng.integers(3 * m - 1))
+        kind = c % 6
+        if kind == 0:          # well formed: an adjacent swap
+            o[i, a], o[i, a + 1] = o[i, a + 1], o[i, a]
+        elif kind == 1:        # duplicate op (and one op missing)
+            o[i, a + 1] = o[i, a]
+        elif kind == 2:        # op kind 3 does not exist
+            o[i, a] = (o[i, a] & ~np.uint16(3)) | np.uint16(3)
+        elif kind == 3:        # microbatch out of range
+            o[i, a] = np.uint16((m + int(rng.integers(0, 4))) << 2)
+        elif kind == 4:        # late damage: the last op of the last stage repeats the first
+            o[P - 1, 3 * m - 1] = o[P - 1, 0]
+        else:                  # offload bit on an F without an offloadable activation
+            if len(not_offl):
+                s, j = not_offl[int(rng.integers(len(not_offl)))]
+                b = int(s) * m + int(j)
+                mk[b >> 5] |= np.uint32(1 << (b & 31))
+            elif len(offl):    # everything offloadable: toggle a real bit instead (well formed)
+                s, j = offl[0]
+                b = int(s) * m + int(j)
+                mk[b >> 5] ^= np.uint32(1 << (b & 31))
+        rows.append(o)
+        masks.append(mk)
+        kinds.append(kind)
+    return np.stack(rows), np.stack(masks), kinds
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+@pytest.mark.parametrize("with_base", [False, True])
+def test_malformed_candidates_match_the_oracle(cuda_ok, cfg, with_base):
+    import torch
+    from oracle.oracle import Oracle
+    from paper_2510_05186_b200.engine import Base
+    inst, pk, base, di = _setup(cfg)
+    orders, masks, kinds = _malformed_batch(pk, base, np.random.default_rng(11 + cfg))
+    b = None
+    if with_base:
+        o0, mk0, _ = base[0]
+        b = Base(di)
+        b.record(torch.from_numpy(o0.view(np.int16)).cuda(), torch.from_numpy(mk0.view(np.int32)).cuda())
+    res = di.evaluate(torch.from_numpy(orders.view(np.int16)).cuda(),
+                      torch.from_numpy(masks.view(np.int32)).cuda(), peak=True, base=b)
+    want = Oracle(pk).eval_batch(orders, masks)
+    flags = res.flags.cpu().numpy().astype(np.uint32)
+    assert (flags == want["flags"]).all(), (cfg, with_base, list(zip(kinds, flags, want["flags"])))
+    # every damaged candidate is flagged malformed, never scheduled
+    for k, f in zip(kinds, flags):
+        if k in (1, 2, 3, 4):
+            assert f == 4, (k, f)
+    ok = want["flags"] == 1
+    assert (res.makespan.cpu().numpy()[ok] == want["makespan"][ok]).all()
+    assert (res.peak.cpu().numpy()[ok] == want["peak"][ok]).all()
+
+
+def test_host_path_flags_malformed_candidates(cuda_ok):
+    from oracle.oracle import Oracle
+    inst, pk, base, di = _setup(2)
+    orders, masks, _ = _malformed_batch(pk, base, np.random.default_rng(5))
+    res = di.evaluate_host(orders.astype(np.uint8) if pk.num_microbatches <= 64 else orders, masks)
+    want = Oracle(pk).eval_batch(orders, masks)
+    assert (res.flags.astype(np.uint32) == want["flags"]).all()
+    ok = want["flags"] == 1
+    assert (res.makespan[ok] == want["makespan"][ok]).all()
+
+
+def test_empty_batches(cuda_ok):
+    import torch
+    inst, pk, base, di = _setup(2)
+    P, stride, w = pk.num_stages, pk.order_stride, pk.mask_words
+    res = di.evaluate(torch.zeros((0, P, stride), dtype=torch.int16, device="cuda"),
+                      torch.zeros((0, w), dtype=torch.int32, device="cuda"), peak=True)
+    torch.cuda.synchronize()
+    assert res.makespan.numel() == 0 and res.flags.numel() == 0
+    out = di.evaluate_host(np.zeros((0, P, stride), np.uint16), np.zeros((0, w), np.uint32))
+    assert out.makespan.shape == (0,)
+
+
+def test_drop_in_run_order_rejects_malformed_structures(cuda_ok):
+    """The drop-in validates structure on the host like encode_candidate: a duplicate op is a
+    ValueError, offloading an op without an activation is the reference's KeyError."""
+    from paper_2510_05186_b200 import listsched, workloads
+    from paper_2510_05186_b200.heuristics import generator_structures
+    inst = workloads.config2()
+    orders, off = generator_structures(inst)[0]
+    bad = dict(orders)
+    row = list(bad[1])
+    row[1] = row[0]
+    bad[1] = tuple(row)
+    with pytest.raises(ValueError):
+        listsched.run_order(inst, bad, off)
+    from paper_2510_05186_b200.instance import OpId, OpKind
+    with pytest.raises(KeyError):
+        listsched.run_order(inst, orders, set(off) | {OpId(1, 1, OpKind.B)})
