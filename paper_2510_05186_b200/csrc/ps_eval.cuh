@@ -167,6 +167,9 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #else
 #define PS_NOUNROLL_C
 #endif
+#ifndef PS_MIN_BLOCKS_G
+#define PS_MIN_BLOCKS_G 4     // global-memory state (config 5): four 4-warp blocks per SM, 122 registers (r01 A/B: 1 -> 4 is 48.9 -> 35.5 ms per round)
+#endif
 #ifndef PS_MIN_BLOCKS_MAT
 #define PS_MIN_BLOCKS_MAT 5   // materialised candidates: 102-register cap (r01 A/B)
 #endif
@@ -176,7 +179,7 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
 template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__(128, (GSTATE || REC) ? 1 : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
+__global__ void __launch_bounds__(128, REC ? 1 : GSTATE ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
