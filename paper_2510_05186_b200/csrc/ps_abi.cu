@@ -188,35 +188,56 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     if (!pl->gstate && (size_t)(pl->inc_words + pl->warps * pl->cand_words) * 4 * 2 > (size_t)I->max_smem_optin &&
         pl->warps <= 2 && env_int("PS_FORCE_SMEM", 0) == 0)
         pl->gstate = true;
-    if (pl->gstate) {
+    // resident blocks per SM of a plan (cached occupancy answers: one query per shape)
+    auto blocks_per_sm = [&](int *per_sm) -> int {
+        Variant v;
+        v.gstate = pl->gstate;
+        v.record = false;
+        v.derived = true;
+        v.uni = I->uniform != 0;
+        const uint64_t okey = ((uint64_t)pl->cfg.smem << 16) | ((uint64_t)pl->cfg.block << 2) |
+                              ((uint64_t)pl->gstate << 1) | (uint64_t)moves;
+        *per_sm = 0;
+        {
+            std::lock_guard<std::mutex> lk(I->occ_mu);
+            auto it = I->occ_cache.find(okey);
+            if (it != I->occ_cache.end()) *per_sm = it->second;
+        }
+        if (*per_sm == 0) {
+            cudaError_t e = occupancy(I->v64, moves, v, pl->cfg.block, pl->cfg.smem, per_sm);
+            if (e != cudaSuccess) return cuda_fail(e, "occupancy");
+            std::lock_guard<std::mutex> lk(I->occ_mu);
+            I->occ_cache[okey] = *per_sm > 0 ? *per_sm : 1;
+        }
+        if (*per_sm < 1) *per_sm = 1;
+        return PS_OK;
+    };
+    auto use_gstate = [&]() {
         // global-memory state. Move mode: the warps of a block share one shared-memory copy of
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
+        pl->gstate = true;
         pl->warps = moves ? std::max(1, std::min(4, env_int("PS_GSTATE_WARPS", 4))) : 1;
         pl->cfg.smem = (size_t)pl->inc_words * 4;
+        pl->cfg.block = 32 * pl->warps;
+    };
+    int per_sm = 0, rc;
+    if (pl->gstate) {
+        use_gstate();
+    } else {
+        pl->cfg.block = 32 * pl->warps;
+        if ((rc = blocks_per_sm(&per_sm)) != PS_OK) return rc;
+        // Shared-memory state that leaves fewer than PS_GSTATE_BELOW_WARPS warps resident per SM
+        // loses to L1/L2-resident global scratch at 16 warps (config 4, 16 x 128: 2 blocks of 4
+        // warps per SM, 7.96 vs 5.61 ms per 65,536-neighbour round; configs 2 and 3 keep 28 warps
+        // in shared memory, where global state is 30-50% slower; r01 tools/ab_force_g.sh). The
+        // materialised config-4 kernel fits one 4-warp block per SM: e2e 25.4 -> 16.5 ms per step.
+        if (env_int("PS_GSTATE_RULE", 1) && env_int("PS_FORCE_SMEM", 0) == 0 &&
+            per_sm * pl->warps < env_int("PS_GSTATE_BELOW_WARPS", 12))
+            use_gstate();
     }
     if (pl->cfg.smem > (size_t)I->max_smem_optin)
         return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
-    pl->cfg.block = 32 * pl->warps;
-    int per_sm = 0;
-    Variant v;
-    v.gstate = pl->gstate;
-    v.record = false;
-    v.derived = true;
-    v.uni = I->uniform != 0;
-    const uint64_t okey = ((uint64_t)pl->cfg.smem << 16) | ((uint64_t)pl->cfg.block << 2) |
-                          ((uint64_t)pl->gstate << 1) | (uint64_t)moves;
-    {
-        std::lock_guard<std::mutex> lk(I->occ_mu);
-        auto it = I->occ_cache.find(okey);
-        if (it != I->occ_cache.end()) per_sm = it->second;
-    }
-    if (per_sm == 0) {
-        cudaError_t e = occupancy(I->v64, moves, v, pl->cfg.block, pl->cfg.smem, &per_sm);
-        if (e != cudaSuccess) return cuda_fail(e, "occupancy");
-        std::lock_guard<std::mutex> lk(I->occ_mu);
-        I->occ_cache[okey] = per_sm > 0 ? per_sm : 1;
-    }
-    if (per_sm < 1) per_sm = 1;
+    if (pl->gstate && (rc = blocks_per_sm(&per_sm)) != PS_OK) return rc;
     int64_t want = (N + pl->warps - 1) / pl->warps;
     int64_t cap = pl->gstate ? std::min<int64_t>(per_sm, env_int("PS_GSTATE_BLOCKS_PER_SM", 16)) * I->num_sms
                              : (int64_t)per_sm * I->num_sms;

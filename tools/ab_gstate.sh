@@ -1,3 +1,5 @@
+# A/B of the global-state kernel build: tools/ab_gstate.sh (needs build/var/g3.so, g4.so from
+#   python -m paper_2510_05186_b200.build -DPS_MIN_BLOCKS_G=N --out=build/var/gN.so)
 for rep in 1 2; do
 for v in "default 1" "default 4" "build/var/g3.so 4" "build/var/g4.so 4"; do
   set -- $v
