@@ -184,7 +184,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     }
     // A candidate so large that shared memory holds at most 2 per SM (config 5: 32 x 256) runs
     // faster from L2-resident global scratch (per-warp state 70 KB, mostly L1/L2 hits) with 16 warps
-    // per SM: 4-warp blocks sharing the incumbent, 122 registers (PS_MIN_BLOCKS_G).
+    // per SM: one 16-warp block sharing one copy of the incumbent, 122 registers (PS_MIN_BLOCKS_G).
     if (!pl->gstate && (size_t)(pl->inc_words + pl->warps * pl->cand_words) * 4 * 2 > (size_t)I->max_smem_optin &&
         pl->warps <= 2 && env_int("PS_FORCE_SMEM", 0) == 0)
         pl->gstate = true;
@@ -216,7 +216,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         // global-memory state. Move mode: the warps of a block share one shared-memory copy of
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
         pl->gstate = true;
-        pl->warps = moves ? std::max(1, std::min(4, env_int("PS_GSTATE_WARPS", 4))) : 1;
+        pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
         pl->cfg.smem = (size_t)pl->inc_words * 4;
         pl->cfg.block = 32 * pl->warps;
     };

@@ -167,8 +167,11 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #else
 #define PS_NOUNROLL_C
 #endif
+#ifndef PS_GSTATE_MAX_WARPS
+#define PS_GSTATE_MAX_WARPS 16 // global-memory state: warps per block sharing the incumbent copy
+#endif
 #ifndef PS_MIN_BLOCKS_G
-#define PS_MIN_BLOCKS_G 4     // global-memory state (config 5): four 4-warp blocks per SM, 122 registers (r01 A/B: 1 -> 4 is 48.9 -> 35.5 ms per round)
+#define PS_MIN_BLOCKS_G 1     // global-memory state: one 16-warp block per SM, 122 registers (r01 A/B)
 #endif
 #ifndef PS_MIN_BLOCKS_MAT
 #define PS_MIN_BLOCKS_MAT 5   // materialised candidates: 102-register cap (r01 A/B)
@@ -179,7 +182,7 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
 template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__(128, REC ? 1 : GSTATE ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
+__global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 : GSTATE ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
