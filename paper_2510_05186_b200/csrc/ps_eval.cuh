@@ -132,6 +132,27 @@ __device__ __forceinline__ void warp_copy_words(uint32_t *dst, const uint32_t *s
     for (int k = (n4 << 2) + lane; k < n; k += 32) dst[k] = src[k];
 }
 
+// Global-state copies: U independent 16-byte loads in flight per lane before their stores (the
+// rolled loop above exposes one L2 round trip per 512 bytes; config 5 restores 68 KB per neighbour).
+template <int U>
+__device__ __forceinline__ void warp_copy_words_mlp(uint32_t *dst, const uint32_t *src, int n, int lane) {
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    const int n4 = n >> 2;
+    int k = lane;
+#pragma unroll 1
+    for (; k + 32 * (U - 1) < n4; k += 32 * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = s4[k + 32 * u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d4[k + 32 * u] = v[u];
+    }
+#pragma unroll 1
+    for (; k < n4; k += 32) d4[k] = s4[k];
+    for (int q = (n4 << 2) + lane; q < n; q += 32) dst[q] = src[q];
+}
+
 __device__ __forceinline__ unsigned long long make_key(uint32_t hi, uint32_t lo) {
     return ((unsigned long long)hi << 32) | lo;
 }
@@ -169,6 +190,12 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #endif
 #ifndef PS_GSTATE_MAX_WARPS
 #define PS_GSTATE_MAX_WARPS 16 // global-memory state: warps per block sharing the incumbent copy
+#endif
+#ifndef PS_GSTATE_VEC_CMP
+#define PS_GSTATE_VEC_CMP 0   // 16-byte loads in the convergence compare (r01: neutral config 5, -20% config 4)
+#endif
+#ifndef PS_GSTATE_COPY_MLP
+#define PS_GSTATE_COPY_MLP 8  // global-state checkpoint restore: 16-byte loads in flight per lane (r01: 1 -> 8 is -7% config 5)
 #endif
 #ifndef PS_MIN_BLOCKS_G
 #define PS_MIN_BLOCKS_G 1     // global-memory state: one 16-warp block per SM, 122 registers (r01 A/B)
@@ -661,6 +688,38 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         // be irrelevant in the candidate too (dom_bound); state-only words must be equal
         const uint32_t d4 = (uint32_t)d << 2;
         const int n2 = 2 * P * m;
+        if (GSTATE && PS_GSTATE_VEC_CMP) {
+            // same test, four words per lane per 16-byte load (state and checkpoint are 16-byte aligned)
+            for (int k0 = 0; k0 < n2; k0 += 128) {
+                const int kb = k0 + 4 * lane;
+                uint32_t cws[4], bws[4];
+                if (kb + 3 < n2) {
+                    const uint4 c4 = *reinterpret_cast<const uint4 *>(&SW(o_A + (kb)));
+                    const uint4 b4 = *reinterpret_cast<const uint4 *>(src + kb);
+                    cws[0] = c4.x; cws[1] = c4.y; cws[2] = c4.z; cws[3] = c4.w;
+                    bws[0] = b4.x; bws[1] = b4.y; bws[2] = b4.z; bws[3] = b4.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        cws[q] = kb + q < n2 ? SW(o_A + (kb + q)) : 0u;
+                        bws[q] = kb + q < n2 ? src[kb + q] : 0u;
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t cw = cws[q], bw = bws[q];
+                    const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
+                    bool ok = (timed_c == timed_b) && (timed_c ? cw - bw == d4 : cw == bw);
+                    const bool relax = !ok && timed_c && !timed_b && (cw & 3u) == bw;
+                    if (__any_sync(0xffffffffu, relax)) {
+                        const int bound = dom_bound(relax, kb + q, cw);
+                        if (relax) ok = bound != INT_MAX && (int)(cw >> 2) <= bound;
+                    }
+                    eq = eq && ok;
+                }
+                if ((k0 & 1023) == 896 && !__all_sync(0xffffffffu, eq)) return false;
+            }
+        } else
         for (int k0 = 0; k0 < n2; k0 += 32) {
             const int k = k0 + lane;
             uint32_t cw = 0u, bw = 0u;
@@ -902,7 +961,8 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 __syncwarp();
                 continue;
             }
-            warp_copy_words(&SW(o_A), src, nz, lane);
+            if (GSTATE) warp_copy_words_mlp<PS_GSTATE_COPY_MLP>(&SW(o_A), src, nz, lane);
+            else warp_copy_words(&SW(o_A), src, nz, lane);
             if (has_stage) {
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
