@@ -62,13 +62,14 @@ def test_search_round_matches_cpu_round(cuda_ok):
     assert int(ls.best_key.item()) == best
 
 
-def test_search_round_matches_cpu_round_large(cuda_ok):
-    """Config 5 (32 stages x 256 microbatches; state in global scratch): a round's neighbours
-    with prefix/suffix sharing against the recorded incumbent vs the CPU restatement."""
+@pytest.mark.parametrize("cfg,n", [(5, 24), (4, 256)])
+def test_search_round_matches_cpu_round_large(cuda_ok, cfg, n):
+    """Configs 5 (32 x 256) and 4 (16 x 128), whose search rounds keep per-candidate state in
+    global scratch (16-warp blocks sharing the incumbent): a round's neighbours with prefix/suffix
+    sharing against the recorded incumbent vs the CPU restatement."""
     import torch
     from oracle.oracle import Oracle
-    inst, orders, off, LocalSearch, SearchConfig = _setup(5)
-    n = 24
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
     ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
                                                      max_shift=MAXSHIFT))
     ms = torch.empty(n, dtype=torch.int64, device="cuda")
