@@ -192,7 +192,10 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #define PS_GSTATE_MAX_WARPS 16 // global-memory state: warps per block sharing the incumbent copy
 #endif
 #ifndef PS_GSTATE_VEC_CMP
-#define PS_GSTATE_VEC_CMP 0   // 16-byte loads in the convergence compare (r01: neutral config 5, -20% config 4)
+#define PS_GSTATE_VEC_CMP 0   // convergence-compare load schedule for global state: 1 = 16-byte loads, 2 = rows in flight
+#endif
+#ifndef PS_GSTATE_CMP_U
+#define PS_GSTATE_CMP_U 4
 #endif
 #ifndef PS_GSTATE_COPY_MLP
 #define PS_GSTATE_COPY_MLP 8  // global-state checkpoint restore: 16-byte loads in flight per lane (r01: 1 -> 8 is -7% config 5)
@@ -688,7 +691,31 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         // be irrelevant in the candidate too (dom_bound); state-only words must be equal
         const uint32_t d4 = (uint32_t)d << 2;
         const int n2 = 2 * P * m;
-        if (GSTATE && PS_GSTATE_VEC_CMP) {
+        if (GSTATE && PS_GSTATE_VEC_CMP == 2) {
+            // same test, PS_GSTATE_CMP_U coalesced rows of loads in flight before they are tested
+            constexpr int U = PS_GSTATE_CMP_U;
+            for (int k0 = 0; k0 < n2; k0 += 32 * U) {
+                uint32_t cws[U], bws[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = k0 + 32 * u + lane;
+                    cws[u] = k < n2 ? SW(o_A + (k)) : 0u;
+                    bws[u] = k < n2 ? src[k] : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t cw = cws[u], bw = bws[u];
+                    const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
+                    bool ok = (timed_c == timed_b) && (timed_c ? cw - bw == d4 : cw == bw);
+                    const bool relax = !ok && timed_c && !timed_b && (cw & 3u) == bw;
+                    if (__any_sync(0xffffffffu, relax)) {
+                        const int bound = dom_bound(relax, k0 + 32 * u + lane, cw);
+                        if (relax) ok = bound != INT_MAX && (int)(cw >> 2) <= bound;
+                    }
+                    eq = eq && ok;
+                }
+            }
+        } else if (GSTATE && PS_GSTATE_VEC_CMP == 1) {
             // same test, four words per lane per 16-byte load (state and checkpoint are 16-byte aligned)
             for (int k0 = 0; k0 < n2; k0 += 128) {
                 const int kb = k0 + 4 * lane;
