@@ -71,19 +71,38 @@ def adapt_batch(entries, inst, device=None) -> list:
         if _shape(e) != (inst.num_stages, inst.num_microbatches):
             raise ShapeMismatch(f"entry is {_shape(e)[0]}x{_shape(e)[1]}, instance is "
                                 f"{inst.num_stages}x{inst.num_microbatches}")
-    cands = []
+    cands, slots = [], []
     for e in entries:
         orders = {i + 1: tuple(e.stage_orders[i]) for i in range(len(e.stage_orders))}
         chans = {g: tuple(e.channel_orders[g]) for g in range(len(e.channel_orders))}
-        cands.append((orders, frozenset(e.offloaded), chans))
+        # an entry recorded under another topology (the cache key ignores topology_groups) is
+        # not adaptable here: ChannelMismatch, DESIGN.md §7
+        if _channels_match(inst, chans):
+            slots.append(len(cands))
+            cands.append((orders, frozenset(e.offloaded), chans))
+        else:
+            slots.append(None)
     res = run_orders(inst, cands, explicit=True, device=device) if cands else []
     out = []
-    for r in res:
-        if isinstance(r, OrderInfeasible) or not validate(r, inst, MemorySemantics.STRICT).ok:
+    for k in slots:
+        r = None if k is None else res[k]
+        if r is None or isinstance(r, OrderInfeasible) or not validate(r, inst, MemorySemantics.STRICT).ok:
             out.append(None)
         else:
             out.append(r)
     return out
+
+
+def _channels_match(inst, chans) -> bool:
+    """Every listed transfer belongs to a stage the instance serves on that channel."""
+    n = len(inst.topology_groups)
+    for g, seq in chans.items():
+        if g >= n:
+            continue                     # channels the instance lacks are never read (listsched.py:233)
+        for op, _kind in seq:
+            if not (1 <= op[0] <= inst.num_stages) or inst.stage_channel(op[0]) != g:
+                return False
+    return True
 
 
 def adapt(entry, inst, device=None):

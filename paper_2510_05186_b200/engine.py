@@ -110,6 +110,7 @@ class DeviceInstance:
         """Device tensors in, device tensors out; asynchronous on `stream`.  With a recorded
         `base`, candidates resume from its last checkpoint before they first differ from it."""
         n = int(orders.shape[0])
+        self._check_batch(n, orders, masks, chans, host=False)
         res = out if out is not None else self.alloc_results(n, peak=peak, trace=trace)
         cb, rb = self._batch_structs(n, orders, masks, chans, res, base)
         N.check(self.lib.ps_eval_batch(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
@@ -126,10 +127,50 @@ class DeviceInstance:
                              np.empty((n, self.P), np.int64) if peak else None, np.empty(n, np.int32),
                              np.empty((n, E), np.int32) if trace else None,
                              np.empty((n, E), np.int32) if trace else None)
-        cb, rb = self._batch_structs(n, np.ascontiguousarray(orders), np.ascontiguousarray(masks),
-                                     None if chans is None else np.ascontiguousarray(chans), out, base)
+        # the library reads these through raw pointers during the call: keep the (possibly
+        # converted) arrays bound to locals until it returns
+        h_orders, h_masks, h_chans = self._check_batch(n, orders, masks, chans, host=True)
+        cb, rb = self._batch_structs(n, h_orders, h_masks, h_chans, out, base)
         N.check(self.lib.ps_eval_batch_host(self.handle, C.byref(cb), C.byref(rb), self._stream(stream)))
+        del h_orders, h_masks, h_chans
         return out
+
+    def _check_batch(self, n, orders, masks, chans, host):
+        """Shapes and element types the C ABI reads (include/pipesched_b200.h ps_cand_batch):
+        orders [N][P][order_stride] of uint16 (or uint8 when 4m <= 256), masks [N][mask_words]
+        of 32-bit words, channel orders [N][G][width] of 32-bit words, all contiguous."""
+        pk = self.packed
+        if tuple(orders.shape) != (n, pk.num_stages, pk.order_stride):
+            raise ValueError(f"orders must be [{n}, {pk.num_stages}, {pk.order_stride}], got {tuple(orders.shape)}")
+        if tuple(masks.shape) != (n, pk.mask_words):
+            raise ValueError(f"masks must be [{n}, {pk.mask_words}], got {tuple(masks.shape)}")
+        if chans is not None and (chans.ndim != 3 or tuple(chans.shape[:2]) != (n, pk.num_channels)):
+            raise ValueError(f"channel orders must be [{n}, {pk.num_channels}, width], got {tuple(chans.shape)}")
+        if host:
+            od = np.dtype(orders.dtype)
+            if od == np.uint8 and 4 * pk.num_microbatches > 256:
+                raise ValueError("uint8 op codes need 4m <= 256")
+            if od not in (np.dtype(np.uint8), np.dtype(np.uint16), np.dtype(np.int16)):
+                raise TypeError(f"orders must be uint8/uint16/int16 op codes, got {od}")
+            if np.dtype(masks.dtype).itemsize != 4 or np.dtype(masks.dtype).kind not in "iu":
+                raise TypeError(f"masks must be 32-bit words, got {masks.dtype}")
+            if chans is not None and (np.dtype(chans.dtype).itemsize != 4 or np.dtype(chans.dtype).kind not in "iu"):
+                raise TypeError(f"channel orders must be 32-bit words, got {chans.dtype}")
+            return (np.ascontiguousarray(orders), np.ascontiguousarray(masks),
+                    None if chans is None else np.ascontiguousarray(chans))
+        import torch
+        if orders.dtype not in (torch.uint8, torch.int16, torch.uint16):
+            raise TypeError(f"orders must be uint8/int16/uint16 op codes, got {orders.dtype}")
+        if orders.dtype == torch.uint8 and 4 * pk.num_microbatches > 256:
+            raise ValueError("uint8 op codes need 4m <= 256")
+        if masks.dtype not in (torch.int32, torch.uint32):
+            raise TypeError(f"masks must be 32-bit words, got {masks.dtype}")
+        if chans is not None and chans.dtype not in (torch.int32, torch.uint32):
+            raise TypeError(f"channel orders must be 32-bit words, got {chans.dtype}")
+        for name, t in (("orders", orders), ("masks", masks), ("channel orders", chans)):
+            if t is not None and (not t.is_cuda or not t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous CUDA tensor")
+        return orders, masks, chans
 
 
 class Base:

@@ -19,6 +19,7 @@ from __future__ import annotations
 import importlib
 
 from . import listsched as _ours
+from .packing import ChannelMismatch
 
 _SITES = ("listsched", "heuristics", "cache")
 _saved: dict = {}
@@ -34,6 +35,10 @@ def gpu_run_order_for(ref_pkg):
             return _ours.run_order(inst, stage_orders, offloaded, channel_orders, types=ref_sched)
         except _ours.OrderInfeasible as e:
             raise ref_ls.OrderInfeasible(str(e), e.stages) from None
+        except ChannelMismatch as e:
+            # an explicit channel order from another topology: not replayable here;
+            # the reference's callers (cache.adapt) treat it as not adaptable
+            raise ref_ls.OrderInfeasible(str(e), ()) from None
 
     run_order.__doc__ = "GPU-evaluated drop-in for pipesched.listsched.run_order (listsched.py:167)."
     return run_order

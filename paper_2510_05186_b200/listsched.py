@@ -15,6 +15,8 @@ the generators and the cache.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 
 from . import _native as N
@@ -71,6 +73,10 @@ def run_orders(inst, candidates, explicit=False, device=None, types=None):
     from .engine import device_instance
     types = types or _sched
     di = device_instance(inst, device)
+    try:
+        inst_ref = weakref.ref(inst)
+    except TypeError:
+        inst_ref = None
     pk = di.packed
     n = len(candidates)
     if n == 0:
@@ -107,7 +113,8 @@ def run_orders(inst, candidates, explicit=False, device=None, types=None):
             metrics = None
             if types is _sched:
                 metrics = _sched.EvalMetrics(int(makespan[c]), float(bubble[c]),
-                                             {i + 1: int(peak[c, i]) for i in range(pk.num_stages)})
+                                             {i + 1: int(peak[c, i]) for i in range(pk.num_stages)},
+                                             inst_ref)
                 out.append(_sched.Schedule.build(comp, trans, cand[1], metrics))
             else:
                 out.append(types.Schedule.build(comp, trans, cand[1]))

@@ -78,6 +78,14 @@ def decode_op(stage0: int, code: int) -> OpId:
     return OpId(stage0 + 1, (code >> 2) + 1, OpKind(code & 3))
 
 
+class ChannelMismatch(ValueError):
+    """An explicit channel order lists a transfer of a stage that the instance's topology serves
+    on another channel.  The reference replays such an order on the listed channel
+    (listsched.py:233-239); the kernels serve each stage's transfers on its own channel only, so
+    the drop-in rejects the order instead: ``cache.adapt_batch`` reports the entry
+    as not adaptable (None) and the integrate wrapper raises the reference's OrderInfeasible."""
+
+
 def _kind_is_reload(kind) -> bool:
     return getattr(kind, "value", kind) == "reload"
 
@@ -132,7 +140,7 @@ def encode_candidate(pk: PackedInstance, stage_orders, offloaded, channel_orders
                 if tuple(op) not in off:
                     raise KeyError(op)
                 if pk.stage_channel[i - 1] != g:
-                    raise ValueError(f"{op} is not served by channel {g}")
+                    raise ChannelMismatch(f"{op} is not served by channel {g}")
                 rel = _kind_is_reload(kind)
                 if (tuple(op), rel) in seen:
                     raise ValueError(f"duplicate transfer {op} on channel {g}")

@@ -85,6 +85,21 @@ def combine_keys(key_tensor, group=None):
     return key_tensor
 
 
+def agree_stop(stop: bool, device, group=None) -> bool:
+    """The ranks' joint stop decision: stop when ANY rank wants to.  Wall-clock budgets are read
+    on each rank's own clock, so without this one rank could leave the loop while another enters
+    one more round and blocks in its all-reduce.  One 4-byte all-reduce(MAX); a no-op at world 1."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return stop
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", device) if backend == "nccl" else torch.device("cpu")
+    flag = torch.tensor([1 if stop else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    return bool(flag.item())
+
+
 def improves(key: int, incumbent_makespan: int) -> bool:
     """Only strict improvements replace the incumbent (solver.py:437 convention)."""
     return key != N.BEST_NONE and unpack_key(key)[0] < incumbent_makespan
@@ -158,6 +173,10 @@ class LocalSearch:
         self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
         return True
 
+    def should_stop(self, local_stop: bool) -> bool:
+        """Collective stop decision (agree_stop) over this search's process group."""
+        return agree_stop(local_stop, self.di.device, self.group) if self.world > 1 else local_stop
+
     def step(self, t0=None) -> bool:
         self.launch_round()
         return self.finish_round(t0)
@@ -179,7 +198,7 @@ class LocalSearch:
         while True:
             if rounds is not None and self.round >= rounds:
                 break
-            if time_budget is not None and time.perf_counter() - t0 >= time_budget:
+            if time_budget is not None and self.should_stop(time.perf_counter() - t0 >= time_budget):
                 break
             if self.step(t0):
                 stale = 0

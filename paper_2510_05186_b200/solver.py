@@ -134,7 +134,9 @@ def start_session(inst: PipelineInstance, budget: SolveBudget | None = None,
         if ls.makespan != span0:
             raise RuntimeError("warm start re-timed to a different makespan")
         while True:
-            if budget.wall_time_limit is not None and _time.monotonic() - t0 >= budget.wall_time_limit:
+            # the wall-clock test is collective: every rank leaves the loop on the same round
+            if budget.wall_time_limit is not None and ls.should_stop(
+                    _time.monotonic() - t0 >= budget.wall_time_limit):
                 break
             if budget.node_limit is not None and nodes + cfg.neighbours > budget.node_limit:
                 break
