@@ -16,9 +16,17 @@ reference's ``OrderInfeasible`` with the same ``stages`` tuple.
 
 from __future__ import annotations
 
+import ctypes as C
 import importlib
+import time
+from dataclasses import dataclass
+
+import numpy as np
 
 from . import listsched as _ours
+from . import _native as N
+from .packing import decode_mask, decode_orders
+from .search import SearchConfig
 from .packing import ChannelMismatch
 
 _SITES = ("listsched", "heuristics", "cache")
@@ -44,7 +52,100 @@ def gpu_run_order_for(ref_pkg):
     return run_order
 
 
-def install(ref_pkg) -> None:
+@dataclass(frozen=True)
+class WarmSearch:
+    """How the GPU local search improves a warm start before the reference solver sees it."""
+
+    config: SearchConfig = SearchConfig()
+    rounds: int | None = None
+    time_budget: float | None = None
+    patience: int | None = 16          # rounds in a row without improvement that end the search
+    device: int | None = None
+
+
+def search_warm_start(ref_pkg, inst, warm=None, search: WarmSearch = WarmSearch()):
+    """Run the GPU local search on a reference instance and return ``(schedule, events)``.
+
+    ``warm`` (a reference ``Schedule``) is the start; by default the reference's own
+    ``best_feasible`` (heuristics.py:196-210 — GPU-timed when installed).  ``schedule`` is the
+    winner as a reference ``Schedule`` (commit-ordered events, STRICT-valid), ready for
+    ``pipesched.start_session(warm=...)`` (solver.py:543-565); ``events`` are the strict
+    improvements as reference ``IncumbentEvent`` objects with the search's timestamps
+    (solver.py:81-87, 435-449), the warm start first at 0.0."""
+    from .search import LocalSearch
+    ref_solver = importlib.import_module(ref_pkg.__name__ + ".solver")
+    ref_sched = importlib.import_module(ref_pkg.__name__ + ".schedule")
+    ref_ls = importlib.import_module(ref_pkg.__name__ + ".listsched")
+    if warm is None:
+        warm, _ = ref_pkg.best_feasible(inst, ref_pkg.AdaParams())
+    span0 = ref_sched.makespan(warm, inst)
+    orders = {i: ref_ls.stage_order_of(warm, i) for i in range(1, inst.num_stages + 1)}
+    ls = LocalSearch(inst, orders, warm.offloaded, search.config, device=search.device)
+    if ls.makespan != span0:
+        raise RuntimeError("warm start re-timed to a different makespan")
+    rounds = search.rounds
+    if rounds is None and search.time_budget is None and search.patience is None:
+        rounds = 64
+    start_orders, start_mask = ls.inc_orders.clone(), ls.inc_mask.clone()
+    res = ls.run(rounds=rounds, time_budget=search.time_budget, patience=search.patience)
+    # every strict improvement as a reference Schedule: replay the winning moves from the warm
+    # structure on the device, then time all the incumbents in one launch
+    structures = []
+    for imp in res.improvements:
+        N.check(ls.lib.ps_apply_move(ls.di.handle, C.c_void_p(start_orders.data_ptr()),
+                                     C.c_void_p(start_mask.data_ptr()), C.byref(ls.moves), imp.round,
+                                     imp.index, ls._stream()))
+        pk = ls.di.packed
+        structures.append((decode_orders(pk, start_orders.cpu().numpy().view(np.uint16)),
+                           decode_mask(pk, start_mask.cpu().numpy().view(np.uint32))))
+    scheds = _ours.run_orders(inst, structures, device=ls.di.device, types=ref_sched) if structures else []
+    from .solver import lower_bound
+    lb = lower_bound(inst, inst.post_validation, device=ls.di.device)
+    events = [ref_solver.IncumbentEvent(warm, span0, min(lb, span0), 0.0)]
+    for imp, sched in zip(res.improvements, scheds):
+        if ref_sched.makespan(sched, inst) != imp.makespan:
+            raise RuntimeError("replayed incumbent re-timed to a different makespan")
+        events.append(ref_solver.IncumbentEvent(sched, imp.makespan, min(lb, imp.makespan), imp.timestamp))
+    return events[-1].schedule, events
+
+
+def search_fed_start_session(ref_pkg, search: WarmSearch = WarmSearch()):
+    """A ``start_session`` with the reference signature (solver.py:543-565) whose warm start is
+    first improved by the GPU local search; the reference branch-and-bound then runs unchanged
+    from the search's winner.  The returned reference ``SolveSession`` streams the search's
+    improvements (their timestamps) followed by the solver's (shifted by the search's time)."""
+    ref_solver = importlib.import_module(ref_pkg.__name__ + ".solver")
+    original = _saved.get((ref_pkg.__name__, "solver.start_session"), ref_solver.start_session)
+
+    def start_session(inst, budget=None, warm=None, symmetry=True, post_validation=None, auto_warm=True):
+        if warm is None and not auto_warm:
+            return original(inst, budget, warm=None, symmetry=symmetry, post_validation=post_validation,
+                            auto_warm=False)
+        t0 = time.monotonic()
+        try:
+            best, events = search_warm_start(ref_pkg, inst, warm, search)
+        except ref_pkg.NoFeasibleSchedule:
+            return original(inst, budget, warm=None, symmetry=symmetry, post_validation=post_validation,
+                            auto_warm=False)
+        spent = time.monotonic() - t0
+        session = original(inst, budget, warm=best, symmetry=symmetry, post_validation=post_validation,
+                           auto_warm=False)
+        # the search's improvements, then the solver's stream (its first event is the winner again,
+        # re-stamped by the solver at its own clock 0)
+        merged = events[:-1]
+        for ev in session.stream():
+            merged.append(ref_solver.IncumbentEvent(ev.schedule, ev.makespan, ev.lower_bound,
+                                                    ev.timestamp + spent, ev.status))
+        return ref_solver.SolveSession(session.outcome, merged)
+
+    start_session.__doc__ = "GPU-search-fed drop-in for pipesched.solver.start_session (solver.py:543)."
+    return start_session
+
+
+def install(ref_pkg, search: WarmSearch | None = None) -> None:
+    """Point the reference's run_order call sites at the GPU evaluator; with ``search``, also
+    let its ``start_session`` (and so ``solve`` and ``online_sim``) start from the GPU local
+    search's winner."""
     fn = gpu_run_order_for(ref_pkg)
     for site in _SITES:
         mod = importlib.import_module(f"{ref_pkg.__name__}.{site}")
@@ -52,6 +153,15 @@ def install(ref_pkg) -> None:
             _saved.setdefault((ref_pkg.__name__, site), mod.run_order)
             mod.run_order = fn
     ref_pkg.run_order = fn
+    if search is not None:
+        ref_solver = importlib.import_module(ref_pkg.__name__ + ".solver")
+        ref_online = importlib.import_module(ref_pkg.__name__ + ".online")
+        _saved.setdefault((ref_pkg.__name__, "solver.start_session"), ref_solver.start_session)
+        _saved.setdefault((ref_pkg.__name__, "online.start_session"), ref_online.start_session)
+        fed = search_fed_start_session(ref_pkg, search)
+        ref_solver.start_session = fed
+        ref_online.start_session = fed
+        ref_pkg.start_session = fed
 
 
 def uninstall(ref_pkg) -> None:
@@ -61,3 +171,9 @@ def uninstall(ref_pkg) -> None:
             mod = importlib.import_module(f"{ref_pkg.__name__}.{site}")
             mod.run_order = _saved.pop(key)
     ref_pkg.run_order = importlib.import_module(ref_pkg.__name__ + ".listsched").run_order
+    for site in ("solver", "online"):
+        key = (ref_pkg.__name__, f"{site}.start_session")
+        if key in _saved:
+            mod = importlib.import_module(f"{ref_pkg.__name__}.{site}")
+            mod.start_session = _saved.pop(key)
+    ref_pkg.start_session = importlib.import_module(ref_pkg.__name__ + ".solver").start_session

@@ -191,8 +191,8 @@ class LocalSearch:
             patience: int | None = None) -> SearchResult:
         """Rounds until `rounds`, `time_budget` seconds or `patience` rounds without improvement."""
         from .listsched import run_order
-        if rounds is None and time_budget is None:
-            raise ValueError("need rounds or time_budget")
+        if rounds is None and time_budget is None and patience is None:
+            raise ValueError("need rounds, time_budget or patience")
         t0 = time.perf_counter()
         stale = 0
         while True:
