@@ -123,6 +123,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -235,7 +247,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": workload_config(args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -373,11 +386,15 @@ def main():
     torch.cuda.synchronize()
     int32_peak = int(probe.item()) / (p0.elapsed_time(p1) / 1e3) / 1e12
     achieved = ops_per_launch / kern_s / 1e12
-    traffic = None
+    # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the committed ncu --set full
+    # capture of the same command (ncu cannot run inside the timed bench)
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_eval_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            doc = json.load(open(prof))
+            traffic = doc.get("dram_bytes_per_launch")
+            traffic_src = f"profiles/ncu_eval_summary.json (round {doc.get('round')}, {doc.get('kernel')})"
         except Exception:
             traffic = None
     n_cand = cfg.neighbours // world
@@ -389,7 +406,7 @@ def main():
         pass
     line["roofline"] = {
         "bound": "int32-issue", "achieved": achieved, "peak": int32_peak, "unit": "Tops/s",
-        "frac": achieved / int32_peak, "traffic": traffic,
+        "frac": achieved / int32_peak, "traffic": traffic, "traffic_source": traffic_src,
         "kernel": "ps::eval_kernel<int, moves, smem state, derived channels, symmetric tables> (search round)",
         "kernel_ms_per_launch": 1000 * kern_s, "kernel_share_of_step": sum(kern_ms) / sum(step_ms),
         "algorithmic_events_per_launch": ev_full / K, "simulated_events_per_launch": ev_sim / K,
@@ -400,8 +417,10 @@ def main():
                 "peak_gbs": hbm_peak, "peak_gbs_source": hbm_src,
                 "note": "not the binding roof: move-encoded candidates"},
         "note": "latency-bound discrete-event simulation (SURVEY.md 8(d)): achieved counts the algorithmic "
-                "work of every evaluated candidate (10 int ops x its 3Pm + 2|off| events); prefix and suffix "
-                "sharing simulate only simulated_events_per_launch of them"}
+                "work of every evaluated candidate (10 int ops x its 3Pm + 2|off| events for a feasible one; a "
+                "deadlocked one only with the events committed before the deadlock was concluded, a lower "
+                "bound of what the reference commits before it raises); prefix and suffix sharing simulate "
+                "only simulated_events_per_launch of them"}
 
     # ---- e2e through the C ABI with host buffers --------------------------------------------------
     if not args.no_e2e:
@@ -447,6 +466,29 @@ def main():
                        "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate"}
         e2e_flags = outs["flags"].numpy().copy()
         e2e_span = outs["makespan"].numpy().copy()
+        # the same batch as a generic one: no recorded base, every candidate simulated from its
+        # first event, like the CPU port (the like-for-like ratio against cpu_baseline)
+        cb0 = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0, None, 1 if u8 else 2)
+        N.check(lib.ps_eval_batch_host(di.handle, C.byref(cb0), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+        k0 = max(1, min(K, 5))
+        n_ms = []
+        for k in range(k0):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            N.check(lib.ps_eval_batch_host(di.handle, C.byref(cb0), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+            n_ms.append(1000 * (time.perf_counter() - t0))
+        n_tot = torch.tensor([sum(n_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(n_tot, op=dist.ReduceOp.MAX)
+        same = bool((outs["makespan"].numpy() == e2e_span).all() and (outs["flags"].numpy() == e2e_flags).all())
+        line["e2e_no_base"] = {"value": n_cand * world * k0 / (float(n_tot.item()) / 1e3), "unit": UNIT,
+                               "steps": k0, "ms_per_step": float(n_tot.item()) / k0,
+                               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                               "outputs_equal_to_e2e": same,
+                               "note": "ps_eval_batch_host without a recorded base: no prefix/suffix sharing, "
+                                       "each candidate simulated in full (like the CPU port); e2e above resumes "
+                                       "from the incumbent's checkpoints"}
     else:
         line["e2e"] = None
 
@@ -475,6 +517,7 @@ def main():
         gpu_ms = ms_gpu.cpu().numpy()
         mism = int((gpu_ms[:n] != ms_cpu).sum())
         line["cpu_baseline"] = {"value": n / cpu_s, "unit": UNIT, "cores": threads, "kind": "port",
+                                "cpu_model": cpu_model(),
                                 "sample": f"first {n} of {n_cand} neighbours of round {rnd} "
                                           f"(C restatement of listsched.run_order, oracle/ps_oracle.c)",
                                 "parity": {"checked": n, "makespan_mismatches": mism,
@@ -513,6 +556,51 @@ def main():
             ttb["distinct_move_fraction"] = frac
             ttb["cpu_port_seconds_to_best_estimate_dedup"] = ttb["cpu_port_seconds_to_best_estimate"] * frac
         line["time_to_best"] = ttb
+    # ---- whole search without deduplication: every neighbour of every round simulated, rounds from
+    # the warm start to convergence (the early rounds of `value` are the cheapest ones) ------------
+    if not args.no_ttb:
+        cfg_nd = SearchConfig(seed=SEED, neighbours=PER_GPU * world, dedup=False, **MOVES)
+        ls3 = LocalSearch(inst, orders0, s0.offloaded, cfg_nd, device=local)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        round_ms, stale = [], 0
+        while ls3.round < args.ttb_rounds and stale < 16:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ls3.launch_round()
+            e1.record(stream)
+            stale = 0 if ls3.finish_round() else stale + 1      # (host sync: e1 has completed)
+            round_ms.append(e0.elapsed_time(e1))
+        tot = torch.tensor([sum(round_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        tail = round_ms[-50:]
+        line["value_whole_search"] = {
+            "value": cfg_nd.neighbours * len(round_ms) / (float(tot.item()) / 1e3), "unit": UNIT,
+            "rounds": len(round_ms), "final_makespan": ls3.makespan, "initial_makespan": ls3.initial_makespan,
+            "ms_per_round_mean": float(tot.item()) / len(round_ms),
+            "ms_per_round_last50": sum(tail) / len(tail),
+            "value_last50": cfg_nd.neighbours * len(tail) / (sum(tail) / 1e3),
+            "note": "fresh search from the warm start to 16 rounds without improvement, no move "
+                    "deduplication (every neighbour simulated), device time of each round's "
+                    "generate + evaluate + argmin (+ all-reduce)"}
+    # ---- the Python drop-in per call (encode, one launch, decode into a Schedule) -----------------
+    if rank == 0 and not args.no_ttb:
+        from paper_2510_05186_b200.heuristics import best_feasible as bf
+        from paper_2510_05186_b200.listsched import run_order
+        run_order(inst, orders0, s0.offloaded, device=local)
+        t0 = time.perf_counter()
+        reps = 10
+        for _ in range(reps):
+            run_order(inst, orders0, s0.offloaded, device=local)
+        ro_ms = 1000 * (time.perf_counter() - t0) / reps
+        t0 = time.perf_counter()
+        bf(inst, device=local)
+        bf_ms = 1000 * (time.perf_counter() - t0)
+        line["drop_in"] = {"run_order_ms_per_call": ro_ms, "best_feasible_ms_per_call": bf_ms,
+                           "note": "listsched.run_order / heuristics.best_feasible as a Python caller sees "
+                                   "them: structure encode, one kernel launch, trace decode into a Schedule"}
     line["search"] = {"initial_makespan": ls.initial_makespan, "final_makespan": ls.makespan,
                       "warm_start": gen_name, "rounds": ls.round,
                       "improvements": [[imp.round, imp.makespan] for imp in ls.improvements]}

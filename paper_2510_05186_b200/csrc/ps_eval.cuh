@@ -532,8 +532,15 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     };
 
     // Lane 0 publishes a candidate's outcome (search rounds may pass no arrays).
-    auto put_result = [&](uint32_t flag, long long span, uint32_t blocked_mask) {
+    // full_ev: the candidate's algorithmic event count 3Pm + 2|off| (roofline numerator, credited
+    // to feasible outcomes); a deadlocked candidate is credited only with the events the reference
+    // commits before it raises, of which `dl_ev` (committed here, or by the base it matched) is a
+    // lower bound.
+    int full_ev = 0;
+    auto put_result = [&](uint32_t flag, long long span, uint32_t blocked_mask, int dl_ev) {
         if (p.events_total && ecount > ecount0) atomicAdd(p.events_total, (unsigned long long)(ecount - ecount0));
+        if (p.events_total && (flag & (FLAG_FEASIBLE | FLAG_DEADLOCK)))
+            atomicAdd(p.events_total + 1, (unsigned long long)(flag == FLAG_FEASIBLE ? full_ev : max(dl_ev, 0)));
         if (p.flags) p.flags[cand] = flag;
         if (p.makespan) p.makespan[cand] = span;
         if (p.bubble)
@@ -914,7 +921,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             }
         }
         if (__any_sync(0xffffffffu, bad)) {
-            if (lane == 0) put_result(FLAG_MALFORMED, -1LL, 0u);
+            if (lane == 0) put_result(FLAG_MALFORMED, -1LL, 0u, 0);
             if (REC && lane == 0) {
                 // a malformed base is unusable (and must not leave the previous one's tables live)
                 p.base_info[0] = -1;
@@ -927,7 +934,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         if (p.events_total) {
             // the candidate's own event count: 3Pm computes and two transfers per offloaded F
             const int n_off = __reduce_add_sync(0xffffffffu, has_stage ? cand_unrel : 0);
-            if (lane == 0) atomicAdd(p.events_total + 1, (unsigned long long)(3 * P * m + 2 * n_off));
+            full_ev = 3 * P * m + 2 * n_off;
         }
         // ---- prefix sharing: the first step whose inputs differ from the recorded base ----
         uint32_t div = 0u;
@@ -965,7 +972,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 if (lane == 0) {
                     ecount = ecount0 = 0;
                     const long long span = p.base_res[0];
-                    put_result((uint32_t)p.base_info[1], span, (uint32_t)p.base_info[3]);
+                    put_result((uint32_t)p.base_info[1], span, (uint32_t)p.base_info[3], p.base_info[2]);
                     if (MOVES && p.best_key && span >= 0) {
                         long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
                         if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
@@ -1266,7 +1273,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 else span = (long long)__reduce_max_sync(0xffffffffu, hi) - (long long)__reduce_min_sync(0xffffffffu, fs);
             }
             if (lane == 0) {
-                put_result(fl, span, (uint32_t)p.base_info[3]);
+                put_result(fl, span, (uint32_t)p.base_info[3], p.base_info[2] - eoff);
                 if (MOVES && p.best_key && span >= 0) {
                     long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
                     if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
@@ -1276,7 +1283,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             continue;
         }
         if (early_dl) {
-            if (lane == 0) put_result(FLAG_DEADLOCK, -1LL, 0u);
+            if (lane == 0) put_result(FLAG_DEADLOCK, -1LL, 0u, ecount);
             if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = -1;
             __syncwarp();
             continue;
@@ -1345,14 +1352,14 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             const long long span = (long long)hi - (long long)lo;
             if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = (long long)peak * p.unit;
             if (lane == 0) {
-                put_result(FLAG_FEASIBLE, span, 0u);
+                put_result(FLAG_FEASIBLE, span, 0u, 0);
                 if (MOVES && p.best_key) {
                     long long key = (span << 32) | (long long)(uint32_t)(p.first_index + cand);
                     if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
                 }
             }
         } else {
-            if (lane == 0) put_result(FLAG_DEADLOCK, -1LL, rem);
+            if (lane == 0) put_result(FLAG_DEADLOCK, -1LL, rem, ecount);
             if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = -1;
         }
         __syncwarp();
