@@ -160,25 +160,30 @@ int or_run_order(const or_instance *I, const uint16_t *orders, int32_t stride, c
     out->flags = 0;
     out->blocked = 0;
     out->n_events = 0;
-    /* structural checks: permutation rows, offload bits only on offloadable F ops */
+    /* structural checks: every op code names an op of its stage (a row may be shorter than 3m —
+     * terminated by OR_END — or repeat ops: run_order replays such rows literally, committing a
+     * repeated op again, and ends in OrderInfeasible since some op is never committed,
+     * listsched.py:206-252); offload bits only on offloadable F ops (KeyError in the reference) */
     uint8_t *offl = (uint8_t *)calloc((size_t)P * m, 1);
-    uint8_t *seen = (uint8_t *)calloc((size_t)P * m * 3, 1);
+    int *row_len = (int *)malloc((size_t)P * sizeof(int));
     int n_off = 0, bad = 0;
-    for (int i = 0; i < P && !bad; ++i)
+    for (int i = 0; i < P && !bad; ++i) {
+        row_len[i] = Lo;
         for (int q = 0; q < Lo; ++q) {
             uint32_t c = orders[(size_t)i * stride + q];
+            if (c == OR_END) { row_len[i] = q; break; }
             uint32_t j = c >> 2, k = c & 3;
-            if (j >= (uint32_t)m || k > 2 || seen[((size_t)i * m + j) * 3 + k]) { bad = 1; break; }
-            seen[((size_t)i * m + j) * 3 + k] = 1;
+            if (j >= (uint32_t)m || k > 2) { bad = 1; break; }
         }
+    }
     for (int b = 0; b < P * m; ++b)
         if ((mask[b >> 5] >> (b & 31)) & 1u) {
             if (I->act[b] <= 0) bad = 1;
             offl[b] = 1;
             n_off++;
         }
-    free(seen);
     if (bad) {
+        free(row_len);
         free(offl);
         out->flags = 4;
         return 0;
@@ -234,7 +239,7 @@ int or_run_order(const or_instance *I, const uint16_t *orders, int32_t stride, c
         cand best = {0, 0, 0, 0, 0, 0, 0};
         int have = 0;
         for (int i = 0; i < P; ++i) {                            /* stage heads (217-232) */
-            if (stage_pos[i] >= Lo) continue;
+            if (stage_pos[i] >= row_len[i]) continue;
             uint32_t c = orders[(size_t)i * stride + stage_pos[i]];
             int j = (int)(c >> 2), k = (int)(c & 3);
             int64_t ready = compute_ready(S, i, j, k, offl);
@@ -281,13 +286,14 @@ int or_run_order(const or_instance *I, const uint16_t *orders, int32_t stride, c
         }
         if (!have) {                                             /* OrderInfeasible (248-252) */
             for (int i = 0; i < P; ++i)
-                if (stage_pos[i] < Lo) out->blocked |= 1u << i;
+                if (stage_pos[i] < row_len[i]) out->blocked |= 1u << i;
             out->flags = 2;
             break;
         }
         uint32_t code = ((uint32_t)best.rank << 30) | ((uint32_t)best.i << 24) | ((uint32_t)best.j << 2) | (uint32_t)best.k;
         if (best.rank == 0) {                                    /* _commit_compute (148-152, 255-259) */
             int64_t end = best.t + I->proc[OP(best.i, best.j, best.k)];
+            if (S->done[OP(best.i, best.j, best.k)] >= 0) n_done--;     /* a repeated op: len(done) stays */
             S->done[OP(best.i, best.j, best.k)] = end;
             ledger_add(&S->mem[best.i], end, I->delta[OP(best.i, best.j, best.k)]);
             stage_pos[best.i]++;
@@ -391,7 +397,7 @@ int or_run_order(const or_instance *I, const uint16_t *orders, int32_t stride, c
         }
     out->n_events = n_ev;
 
-    free(offl); free(S->done); free(S->off_end); free(S->rel_end); free(S->mem); free(S->pool);
+    free(offl); free(row_len); free(S->done); free(S->off_end); free(S->rel_end); free(S->mem); free(S->pool);
     free(S->scratch); free(stage_pos); free(stage_free); free(chan_free); free(chan_pos); free(pend);
     free(npend); free(requested); free(evs);
     return 0;

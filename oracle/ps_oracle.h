@@ -27,6 +27,10 @@
 extern "C" {
 #endif
 
+/* stage-row terminator: a row shorter than 3m ends at the first OR_END (include/pipesched_b200.h
+ * PS_ROW_END) */
+#define OR_END 0xFFFFu
+
 typedef struct or_instance {
     int32_t P, m, G;
     const int64_t *proc;      /* [P][m][3] */

@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr"]
 
-SOURCES = ["ps_abi.cu", "ps_bound.cu"] + [f"ps_eval_{t}_m{m}.cu" for t in ("i32", "i64") for m in (0, 1)]
+SOURCES = ["ps_abi.cu", "ps_bound.cu", "ps_literal.cu"] + [f"ps_eval_{t}_m{m}.cu" for t in ("i32", "i64") for m in (0, 1)]
 
 
 def _inputs():

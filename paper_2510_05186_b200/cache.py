@@ -24,6 +24,10 @@ class ShapeMismatch(Exception):
     """Entry and instance disagree on (stages, micro-batches)."""
 
 
+GRID_STEP = 0.25          # the reference's default ratio grid (cache.py:30)
+NO_GAMMA = -1.0           # ratio sentinel: nothing to offload (cache.py:31)
+
+
 @dataclass(frozen=True)
 class CachedOrder:
     num_stages: int
@@ -32,6 +36,8 @@ class CachedOrder:
     offloaded: frozenset
     channel_orders: tuple     # per channel tuple of (OpId, TransferKind)
     recorded_makespan_ratio: float = 0.0
+    ratios: tuple = ()        # the record's fingerprint (tB/tF, tW/tF, tcomm/tF, toff/tF, limit/gamma)
+    post_validation: bool = False
 
 
 def entry_from_record(d: dict) -> CachedOrder:
@@ -44,7 +50,8 @@ def entry_from_record(d: dict) -> CachedOrder:
                          TransferKind.OFFLOAD if t == "O" else TransferKind.RELOAD)
                         for i, j, c, t in co) for co in order["channels"])
     return CachedOrder(int(d["key"]["P"]), int(d["key"]["m"]), stages, off, chans,
-                       float(d.get("makespan_ratio", 0.0)))
+                       float(d.get("makespan_ratio", 0.0)), tuple(float(x) for x in d["key"].get("ratios", ())),
+                       bool(d["key"].get("post_validation", False)))
 
 
 def load_entries(path) -> list:
@@ -125,6 +132,99 @@ def warm_start_from_entries(entries, inst, params=None, device=None):
     """Best of the adapted entries and the heuristics; the cache wins ties (cache.py:243-259)."""
     from .heuristics import AdaParams, best_feasible
     adapted, _ = best_adapted(entries, inst, device)
+    fallback, name = best_feasible(inst, params or AdaParams(), device=device)
+    if adapted is not None and makespan(adapted, inst) <= makespan(fallback, inst):
+        return adapted, "cache"
+    return fallback, name
+
+
+# -- every entry within the lookup radius (SURVEY.md §8(f) row 2) ---------------------------------
+# The reference's lookup returns the ONE nearest same-shape entry within a grid step and adapts it
+# (cache.py:207-221, 243-259); here every entry within that radius is re-timed in one launch and
+# the best adaptable one is kept.
+
+def _mean(vals):
+    vals = list(vals)
+    return sum(vals) / len(vals) if vals else 0.0
+
+
+def _snap(value, step):
+    return round(round(value / step) * step, 9)
+
+
+def fingerprint(inst, grid_step: float = GRID_STEP):
+    """(P, m, ratios, post_validation): the reference's discretize (cache.py:111-131)."""
+    if grid_step <= 0:
+        raise ValueError("grid_step must be positive")
+    ops = list(inst.ops())           # (kinds compared by value: reference instances carry their own OpKind)
+    tf = _mean(inst.proc_time[op] for op in ops if int(op[2]) == 0)
+    if tf <= 0:
+        raise ValueError("mean forward time is zero")
+    tb = _mean(inst.proc_time[op] for op in ops if int(op[2]) == 1)
+    tw = _mean(inst.proc_time[op] for op in ops if int(op[2]) == 2)
+    gammas = [inst.act_size[x] for x in inst.offloadable_ops()]
+    mem = _snap(_mean(inst.mem_limit.values()) / _mean(gammas), grid_step) if gammas else NO_GAMMA
+    ratios = (_snap(tb / tf, grid_step), _snap(tw / tf, grid_step), _snap(inst.comm_time / tf, grid_step),
+              _snap(inst.offload_time / tf, grid_step), mem)
+    return inst.num_stages, inst.num_microbatches, ratios, bool(inst.post_validation)
+
+
+def _entry_key(e):
+    key = getattr(e, "key", None)
+    if key is not None:                  # a reference CacheEntry
+        return key.num_stages, key.num_microbatches, tuple(key.ratios), bool(key.post_validation)
+    return e.num_stages, e.num_microbatches, tuple(e.ratios), bool(e.post_validation)
+
+
+def _ratio_distance(a, b) -> float:
+    """The reference's _distance (cache.py:198-204): max abs difference, inf across NO_GAMMA."""
+    worst = 0.0
+    for x, y in zip(a, b):
+        if (x == NO_GAMMA) != (y == NO_GAMMA):
+            return float("inf")
+        worst = max(worst, abs(x - y))
+    return worst
+
+
+def within_radius(entries, inst, grid_step: float = GRID_STEP) -> list:
+    """Indices of the entries the reference's lookup would consider (same shape and post-validation
+    flag, ratio distance within one grid step), ranked as lookup ranks them: (distance, recorded
+    makespan ratio), first wins ties.  lookup's hit is the first of them."""
+    P, m, ratios, post = fingerprint(inst, grid_step)
+    ranked = []
+    for k, e in enumerate(entries):
+        eP, em, er, epost = _entry_key(e)
+        if (eP, em, epost) != (P, m, post):
+            continue
+        d = _ratio_distance(er, ratios)
+        if d > grid_step + 1e-9:
+            continue
+        ranked.append((d, e.recorded_makespan_ratio, k))
+    ranked.sort(key=lambda t: t[:2])       # stable: equal ranks keep file order, as lookup's strict <
+    return [k for _, _, k in ranked]
+
+
+def adapt_radius(entries, inst, grid_step: float = GRID_STEP, device=None):
+    """Re-time every entry within the lookup radius in ONE launch.  Returns (best schedule or None,
+    its entry index or None, [(index, schedule or None) in lookup rank order]); the best is the
+    minimum makespan, the better-ranked entry on ties."""
+    idx = within_radius(entries, inst, grid_step)
+    adapted = adapt_batch([entries[k] for k in idx], inst, device) if idx else []
+    best = (None, None, None)
+    for k, s in zip(idx, adapted):
+        if s is None:
+            continue
+        span = makespan(s, inst)
+        if best[0] is None or span < best[0]:
+            best = (span, s, k)
+    return best[1], best[2], list(zip(idx, adapted))
+
+
+def warm_start_from_radius(entries, inst, params=None, grid_step: float = GRID_STEP, device=None):
+    """warm_start_from_cache (cache.py:243-259) over every entry within the radius: the best
+    adapted entry against the heuristics, the cache winning ties."""
+    from .heuristics import AdaParams, best_feasible
+    adapted, _, _ = adapt_radius(entries, inst, grid_step, device)
     fallback, name = best_feasible(inst, params or AdaParams(), device=device)
     if adapted is not None and makespan(adapted, inst) <= makespan(fallback, inst):
         return adapted, "cache"

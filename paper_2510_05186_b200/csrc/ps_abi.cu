@@ -16,6 +16,7 @@
 
 #include "../../include/pipesched_b200.h"
 #include "ps_launch.h"
+#include "ps_literal.h"
 
 using namespace ps;
 
@@ -947,7 +948,19 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
     p.events_total = (unsigned long long *)r->events_total;
     p.ready = ready;
     p.ready_chunk = ready_chunk;
-    return run_eval(I, p, false, stream, b->base);
+    int rc = run_eval(I, p, false, stream, b->base);
+    if (rc) return rc;
+    // Rows that are not permutations (the evaluator flags them malformed) are replayed with the
+    // reference's literal semantics: they end in OrderInfeasible with its blocked stages
+    // (ps_literal.cu).  Scratch for up to 1024 concurrent replays, at most 128 MiB.
+    const size_t slot = literal_slot_bytes(I->P, I->m, I->G);
+    const int slots = (int)std::max<int64_t>(1, std::min<int64_t>({p.N, 1024, (int64_t)((128u << 20) / slot)}));
+    int64_t *scratch = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&scratch, (size_t)slots * slot, stream));
+    cudaError_t e = literal_launch(p, I->v64, scratch, slots, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "literal replay launch");
+    PS_CUDA(cudaFreeAsync(scratch, stream));
+    return PS_OK;
 }
 
 // Pinned host word holding 1: the copy engine writes it behind each chunk as its ready flag.

@@ -16,7 +16,6 @@ reference's ``OrderInfeasible`` with the same ``stages`` tuple.
 
 from __future__ import annotations
 
-import ctypes as C
 import importlib
 import time
 from dataclasses import dataclass
@@ -24,7 +23,6 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import listsched as _ours
-from . import _native as N
 from .packing import decode_mask, decode_orders
 from .search import SearchConfig
 from .packing import ChannelMismatch
@@ -59,7 +57,8 @@ class WarmSearch:
     config: SearchConfig = SearchConfig()
     rounds: int | None = None
     time_budget: float | None = None
-    patience: int | None = 16          # rounds in a row without improvement that end the search
+    patience: int | None = 16          # steps in a row without improving the best that end the search
+    kicks: int | None = None           # ILS restarts (config.kick_moves > 0)
     device: int | None = None
 
 
@@ -84,20 +83,14 @@ def search_warm_start(ref_pkg, inst, warm=None, search: WarmSearch = WarmSearch(
     if ls.makespan != span0:
         raise RuntimeError("warm start re-timed to a different makespan")
     rounds = search.rounds
-    if rounds is None and search.time_budget is None and search.patience is None:
+    if rounds is None and search.time_budget is None and search.patience is None and search.kicks is None:
         rounds = 64
-    start_orders, start_mask = ls.inc_orders.clone(), ls.inc_mask.clone()
-    res = ls.run(rounds=rounds, time_budget=search.time_budget, patience=search.patience)
-    # every strict improvement as a reference Schedule: replay the winning moves from the warm
-    # structure on the device, then time all the incumbents in one launch
-    structures = []
-    for imp in res.improvements:
-        N.check(ls.lib.ps_apply_move(ls.di.handle, C.c_void_p(start_orders.data_ptr()),
-                                     C.c_void_p(start_mask.data_ptr()), C.byref(ls.moves), imp.round,
-                                     imp.index, ls._stream()))
-        pk = ls.di.packed
-        structures.append((decode_orders(pk, start_orders.cpu().numpy().view(np.uint16)),
-                           decode_mask(pk, start_mask.cpu().numpy().view(np.uint32))))
+    ls.keep_structures = True
+    res = ls.run(rounds=rounds, time_budget=search.time_budget, patience=search.patience, kicks=search.kicks)
+    # every strict improvement of the best as a reference Schedule, all timed in one launch
+    pk = ls.di.packed
+    structures = [(decode_orders(pk, o.cpu().numpy().view(np.uint16)), decode_mask(pk, mk.cpu().numpy().view(np.uint32)))
+                  for o, mk in ls.improvement_structures]
     scheds = _ours.run_orders(inst, structures, device=ls.di.device, types=ref_sched) if structures else []
     from .solver import lower_bound
     lb = lower_bound(inst, inst.post_validation, device=ls.di.device)

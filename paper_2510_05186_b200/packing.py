@@ -78,6 +78,9 @@ def decode_op(stage0: int, code: int) -> OpId:
     return OpId(stage0 + 1, (code >> 2) + 1, OpKind(code & 3))
 
 
+ROW_END = 0xFFFF          # stage-row terminator for rows shorter than 3m (include/pipesched_b200.h)
+
+
 class ChannelMismatch(ValueError):
     """An explicit channel order lists a transfer of a stage that the instance's topology serves
     on another channel.  The reference replays such an order on the listed channel
@@ -106,16 +109,19 @@ def encode_candidate(pk: PackedInstance, stage_orders, offloaded, channel_orders
             row = stage_orders[i]
         except KeyError:
             raise KeyError(i) from None
-        if len(row) != 3 * m:
-            raise ValueError(f"stage {i} order has {len(row)} ops, expected {3 * m}")
-        codes = np.fromiter(((op[1] - 1) << 2 | int(op[2]) for op in row), np.int64, 3 * m)
-        stages = np.fromiter((op[0] for op in row), np.int64, 3 * m)
+        n = len(row)
+        if n > 3 * m:
+            raise ValueError(f"stage {i} order has {n} ops, more than the stage's {3 * m}")
+        codes = np.fromiter(((op[1] - 1) << 2 | int(op[2]) for op in row), np.int64, n)
+        stages = np.fromiter((op[0] for op in row), np.int64, n)
         mbs = codes >> 2
         if (stages != i).any() or (mbs < 0).any() or (mbs >= m).any():
             raise ValueError(f"stage {i} order holds ops of another stage or microbatch range")
-        if len(np.unique(codes)) != 3 * m:
-            raise ValueError(f"stage {i} order is not a permutation of its ops")
-        orders_out[i - 1, :3 * m] = codes
+        # a row that repeats ops or is short is replayed literally, as the reference does
+        # (listsched.py:206-252): it ends in OrderInfeasible (ps_literal.cu)
+        orders_out[i - 1, :n] = codes
+        if n < 3 * m:
+            orders_out[i - 1, n] = ROW_END
     mask_out[:] = 0
     for op in offloaded:
         i, j, k = op

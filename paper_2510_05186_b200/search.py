@@ -37,6 +37,15 @@ class SearchConfig:
     max_shift: int = 4
     share_prefix: bool = True        # resume neighbours from checkpoints of the incumbent
     dedup: bool = True               # simulate a move drawn several times in a round once
+    # Iterated local search: after `descent_patience` rounds without improving
+    # the current point, restart the descent from the best structure kicked by `kick_moves`
+    # random moves.  0 = plain descent (a run then ends at convergence or its budget).
+    kick_moves: int = 0
+    descent_patience: int = 16
+
+
+KICK_ROUND_BASE = 1 << 40            # kick k draws its moves from "round" KICK_ROUND_BASE + k
+KICK_TRIES = 64                      # move draws per kick move before the kick gives up
 
 
 @dataclass
@@ -138,6 +147,15 @@ class LocalSearch:
         self.round = 0
         self.evaluated = 0
         self.improvements = []
+        # best structure so far (differs from the current point only after an ILS kick)
+        self.best_makespan = self.makespan
+        self.best_orders = self.inc_orders.clone()
+        self.best_mask = self.inc_mask.clone()
+        self.kicks = 0
+        self.stale = 0               # rounds since the current point last improved
+        # with keep_structures, (orders, mask) device copies of the best at every improvement
+        self.keep_structures = False
+        self.improvement_structures = []
 
     def _stream(self):
         import torch
@@ -156,13 +174,16 @@ class LocalSearch:
             combine_keys(self.best_key, self.group)
 
     def finish_round(self, t0=None) -> bool:
-        """Read the combined key (host sync) and adopt a strict improvement."""
+        """Read the combined key (host sync) and adopt a strict improvement of the current point;
+        an improvement of the best so far is recorded in `improvements`."""
         key = int(self.best_key.item())
         r = self.round
         self.round += 1
         self.evaluated += self.cfg.neighbours
         if not improves(key, self.makespan):
+            self.stale += 1
             return False
+        self.stale = 0
         span, idx = unpack_key(key)
         N.check(self.lib.ps_apply_move(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
                                        C.c_void_p(self.inc_mask.data_ptr()), C.byref(self.moves),
@@ -170,8 +191,48 @@ class LocalSearch:
         if self.base is not None:
             self.base.record(self.inc_orders, self.inc_mask)
         self.makespan = span
-        self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
+        if span < self.best_makespan:
+            self.best_makespan = span
+            self.best_orders.copy_(self.inc_orders)
+            self.best_mask.copy_(self.inc_mask)
+            self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
+            if self.keep_structures:
+                self.improvement_structures.append((self.best_orders.clone(), self.best_mask.clone()))
         return True
+
+    def kick(self) -> int:
+        """ILS restart: the current point becomes the best structure with up to
+        `kick_moves` random moves applied — kick k applies the moves of "round"
+        KICK_ROUND_BASE + k, neighbour indices 0, 1, ... in turn, keeping each one whose result is
+        still feasible, until kick_moves are kept or KICK_TRIES * kick_moves were drawn.  Returns
+        the current point's makespan.  Deterministic: every rank kicks identically."""
+        k = self.cfg.kick_moves
+        self.inc_orders.copy_(self.best_orders)
+        self.inc_mask.copy_(self.best_mask)
+        save_o, save_m = self.inc_orders.clone(), self.inc_mask.clone()
+        span, kept, tries = self.best_makespan, 0, 0
+        rnd = KICK_ROUND_BASE + self.kicks
+        while kept < k and tries < KICK_TRIES * k:
+            N.check(self.lib.ps_apply_move(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
+                                           C.c_void_p(self.inc_mask.data_ptr()), C.byref(self.moves),
+                                           rnd, tries, self._stream()))
+            tries += 1
+            res = self.di.evaluate(self.inc_orders.view(1, *self.inc_orders.shape), self.inc_mask.view(1, -1),
+                                   peak=False)
+            if int(res.flags[0].item()) & N.FLAG_FEASIBLE:
+                kept += 1
+                span = int(res.makespan[0].item())
+                save_o.copy_(self.inc_orders)
+                save_m.copy_(self.inc_mask)
+            else:
+                self.inc_orders.copy_(save_o)
+                self.inc_mask.copy_(save_m)
+        self.kicks += 1
+        self.makespan = span
+        self.stale = 0
+        if self.base is not None:
+            self.base.record(self.inc_orders, self.inc_mask)
+        return span
 
     def should_stop(self, local_stop: bool) -> bool:
         """Collective stop decision (agree_stop) over this search's process group."""
@@ -182,34 +243,47 @@ class LocalSearch:
         return self.finish_round(t0)
 
     def incumbent_structure(self):
+        """The best structure found so far (stage orders, offloaded set)."""
         pk = self.di.packed
-        o = self.inc_orders.cpu().numpy().view(np.uint16)
-        mk = self.inc_mask.cpu().numpy().view(np.uint32)
+        o = self.best_orders.cpu().numpy().view(np.uint16)
+        mk = self.best_mask.cpu().numpy().view(np.uint32)
         return decode_orders(pk, o), decode_mask(pk, mk)
 
+    def step_ils(self, t0=None) -> bool:
+        """One ILS step: a descent round, or a kick when the descent has converged."""
+        if self.cfg.kick_moves > 0 and self.stale >= self.cfg.descent_patience:
+            self.kick()
+            return False
+        return self.step(t0)
+
     def run(self, rounds: int | None = None, time_budget: float | None = None,
-            patience: int | None = None) -> SearchResult:
-        """Rounds until `rounds`, `time_budget` seconds or `patience` rounds without improvement."""
+            patience: int | None = None, kicks: int | None = None) -> SearchResult:
+        """Rounds until `rounds`, `time_budget` seconds, `patience` rounds without improving the
+        best, or (ILS, kick_moves > 0) `kicks` restarts."""
         from .listsched import run_order
-        if rounds is None and time_budget is None and patience is None:
-            raise ValueError("need rounds, time_budget or patience")
+        if rounds is None and time_budget is None and patience is None and kicks is None:
+            raise ValueError("need rounds, time_budget, patience or kicks")
+        if kicks and self.cfg.kick_moves <= 0:
+            raise ValueError("a kick budget needs SearchConfig.kick_moves > 0")
         t0 = time.perf_counter()
-        stale = 0
+        since_best = 0               # steps (rounds and kicks) since the best last improved
         while True:
             if rounds is not None and self.round >= rounds:
                 break
+            # (a kick budget ends once the descent after the last kick has converged)
+            if kicks is not None and self.kicks >= kicks and self.stale >= self.cfg.descent_patience:
+                break
             if time_budget is not None and self.should_stop(time.perf_counter() - t0 >= time_budget):
                 break
-            if self.step(t0):
-                stale = 0
-            else:
-                stale += 1
-                if patience is not None and stale >= patience:
-                    break
+            best_before = self.best_makespan
+            self.step_ils(t0)
+            since_best = 0 if self.best_makespan < best_before else since_best + 1
+            if patience is not None and since_best >= patience:
+                break
         elapsed = time.perf_counter() - t0
         orders, off = self.incumbent_structure()
         sched = run_order(self.inst, orders, off, device=self.di.device)
-        return SearchResult(sched, self.makespan, self.initial_makespan, self.round, self.evaluated,
+        return SearchResult(sched, self.best_makespan, self.initial_makespan, self.round, self.evaluated,
                             elapsed, list(self.improvements))
 
     # -- checkpoint / resume (SURVEY.md §5): the search state is the incumbent, the round and the
@@ -217,7 +291,10 @@ class LocalSearch:
     def state_dict(self) -> dict:
         return {"inc_orders": self.inc_orders.cpu().numpy().view(np.uint16).copy(),
                 "inc_mask": self.inc_mask.cpu().numpy().view(np.uint32).copy(),
+                "best_orders": self.best_orders.cpu().numpy().view(np.uint16).copy(),
+                "best_mask": self.best_mask.cpu().numpy().view(np.uint32).copy(),
                 "round": self.round, "makespan": self.makespan, "initial_makespan": self.initial_makespan,
+                "best_makespan": self.best_makespan, "kicks": self.kicks, "stale": self.stale,
                 "evaluated": self.evaluated, "config": dict(self.cfg.__dict__),
                 "improvements": [(i.round, i.makespan, i.timestamp, i.index) for i in self.improvements]}
 
@@ -232,6 +309,13 @@ class LocalSearch:
         self.initial_makespan = int(state["initial_makespan"])
         self.evaluated = int(state["evaluated"])
         self.improvements = [Improvement(r, m, t, i) for r, m, t, i in state["improvements"]]
+        self.best_orders.copy_(torch.from_numpy(np.asarray(state.get("best_orders", state["inc_orders"]),
+                                                           np.uint16).view(np.int16)))
+        self.best_mask.copy_(torch.from_numpy(np.asarray(state.get("best_mask", state["inc_mask"]),
+                                                         np.uint32).view(np.int32)))
+        self.best_makespan = int(state.get("best_makespan", self.makespan))
+        self.kicks = int(state.get("kicks", 0))
+        self.stale = int(state.get("stale", 0))
         if self.base is not None:
             self.base.record(self.inc_orders, self.inc_mask)
 

@@ -124,7 +124,8 @@ def start_session(inst: PipelineInstance, budget: SolveBudget | None = None,
         return SolveSession(outcome, [])
     span0 = makespan(warm, inst)
     events = [IncumbentEvent(warm, span0, min(lb, span0), 0.0)]
-    cfg = search or SearchConfig()
+    # the engine: iterated local search until the budget is spent
+    cfg = search or SearchConfig(kick_moves=4)
     best, best_span, nodes = warm, span0, 0
     over = (budget.wall_time_limit is not None and budget.wall_time_limit <= 0) or \
            (budget.node_limit is not None and budget.node_limit <= 0)
@@ -140,10 +141,11 @@ def start_session(inst: PipelineInstance, budget: SolveBudget | None = None,
                 break
             if budget.node_limit is not None and nodes + cfg.neighbours > budget.node_limit:
                 break
-            improved = ls.step()
-            nodes += cfg.neighbours
-            if improved:
-                best_span = ls.makespan
+            before = ls.best_makespan
+            ls.step_ils()
+            nodes = ls.evaluated
+            if ls.best_makespan < before:
+                best_span = ls.best_makespan
                 o, off = ls.incumbent_structure()
                 from .listsched import run_order
                 best = run_order(inst, o, off, device=ls.di.device)

@@ -12,6 +12,7 @@ from paper_2510_05186_b200.packing import PAD_CHANNEL, pack_instance
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 CORPORA = ("ref_tests", "fuzz", "configs")
+MALFORMED = "malformed"
 
 
 @lru_cache(maxsize=None)
@@ -34,6 +35,8 @@ def case_arrays(pk, case):
     orders = np.zeros((P, pk.order_stride), np.uint16)
     for i, row in enumerate(case["orders"]):
         orders[i, :len(row)] = row
+        if len(row) < 3 * m:
+            orders[i, len(row)] = 0xFFFF          # short row: terminator (PS_ROW_END)
     mask = np.zeros(pk.mask_words, np.uint32)
     for i, j in case["offloaded"]:
         b = (i - 1) * m + (j - 1)

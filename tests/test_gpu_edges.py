@@ -1,6 +1,9 @@
 """Edge cases of the batch API on the GPU: empty batches, malformed candidates (with and without a
 recorded base, in the register seen-set path m <= 64 and the shared-memory one m > 64), and the
-drop-in's error behaviour.  Every flag is compared with the C oracle's."""
+drop-in's error behaviour.  Rows that repeat an op, miss one or are cut short follow the
+reference (replayed literally, OrderInfeasible with its blocked stages: tests/golden/malformed.json.gz
+recorded by the reference, and the C oracle pinned to it); op codes that name no op stay
+PS_FLAG_MALFORMED."""
 
 import numpy as np
 import pytest
@@ -74,10 +77,13 @@ def test_malformed_candidates_match_the_oracle(cuda_ok, cfg, with_base):
     want = Oracle(pk).eval_batch(orders, masks)
     flags = res.flags.cpu().numpy().astype(np.uint32)
     assert (flags == want["flags"]).all(), (cfg, with_base, list(zip(kinds, flags, want["flags"])))
-    # every damaged candidate is flagged malformed, never scheduled
+    # codes naming no op are malformed; repeated ops end in OrderInfeasible like the reference
     for k, f in zip(kinds, flags):
-        if k in (1, 2, 3, 4):
+        if k in (2, 3):
             assert f == 4, (k, f)
+        elif k in (1, 4):
+            assert f == 2, (k, f)
+    assert (res.blocked.cpu().numpy().astype(np.uint32)[flags == 2] == want["blocked"][flags == 2]).all()
     ok = want["flags"] == 1
     assert (res.makespan.cpu().numpy()[ok] == want["makespan"][ok]).all()
     assert (res.peak.cpu().numpy()[ok] == want["peak"][ok]).all()
@@ -92,6 +98,8 @@ def test_host_path_flags_malformed_candidates(cuda_ok):
     assert (res.flags.astype(np.uint32) == want["flags"]).all()
     ok = want["flags"] == 1
     assert (res.makespan[ok] == want["makespan"][ok]).all()
+    dl = want["flags"] == 2
+    assert (res.blocked.astype(np.uint32)[dl] == want["blocked"][dl]).all()
 
 
 def test_empty_batches(cuda_ok):
@@ -106,19 +114,61 @@ def test_empty_batches(cuda_ok):
     assert out.makespan.shape == (0,)
 
 
-def test_drop_in_run_order_rejects_malformed_structures(cuda_ok):
-    """The drop-in validates structure on the host like encode_candidate: a duplicate op is a
-    ValueError, offloading an op without an activation is the reference's KeyError."""
+def test_drop_in_run_order_on_malformed_structures(cuda_ok):
+    """A row with a repeated op raises OrderInfeasible with the reference's stages; an op of
+    another stage or an overlong row is a ValueError; offloading an op without an
+    activation is the reference's KeyError."""
     from paper_2510_05186_b200 import listsched, workloads
     from paper_2510_05186_b200.heuristics import generator_structures
+    from paper_2510_05186_b200.instance import OpId, OpKind
     inst = workloads.config2()
     orders, off = generator_structures(inst)[0]
     bad = dict(orders)
     row = list(bad[1])
     row[1] = row[0]
     bad[1] = tuple(row)
-    with pytest.raises(ValueError):
+    with pytest.raises(listsched.OrderInfeasible):
         listsched.run_order(inst, bad, off)
-    from paper_2510_05186_b200.instance import OpId, OpKind
+    foreign = dict(orders)
+    foreign[1] = (OpId(2, 1, OpKind.F),) + tuple(orders[1][1:])
+    with pytest.raises(ValueError):
+        listsched.run_order(inst, foreign, off)
     with pytest.raises(KeyError):
         listsched.run_order(inst, orders, set(off) | {OpId(1, 1, OpKind.B)})
+
+
+@pytest.mark.parametrize("explicit", [False, True])
+def test_malformed_rows_match_the_reference(cuda_ok, explicit):
+    """The reference-recorded outcomes of damaged rows (tests/golden/malformed.json.gz) through
+    ps_eval_batch and through the drop-in run_order (OrderInfeasible.stages)."""
+    import torch
+    from _golden import case_arrays, corpus, structure
+    from paper_2510_05186_b200 import listsched
+    from paper_2510_05186_b200.engine import DeviceInstance
+    n = 0
+    for inst, pk, cases in corpus("malformed"):
+        sel = [c for c in cases if ("channel_orders" in c) == explicit]
+        if not sel:
+            continue
+        arrs = [case_arrays(pk, c) for c in sel]
+        chans = None
+        if explicit:
+            width = max(a[2].shape[1] for a in arrs)
+            ch = np.full((len(arrs), pk.num_channels, width), 0xFFFFFFFF, np.uint32)
+            for k, a in enumerate(arrs):
+                ch[k, :, :a[2].shape[1]] = a[2]
+            chans = torch.from_numpy(ch.view(np.int32)).cuda()
+        di = DeviceInstance(inst, packed=pk)
+        res = di.evaluate(torch.from_numpy(np.stack([a[0] for a in arrs]).view(np.int16)).cuda(),
+                          torch.from_numpy(np.stack([a[1] for a in arrs]).view(np.int32)).cuda(), chans, peak=True)
+        flags = res.flags.cpu().numpy()
+        blocked = res.blocked.cpu().numpy().astype(np.uint32)
+        for k, case in enumerate(sel):
+            assert flags[k] == 2, case["damage"]
+            assert [i + 1 for i in range(pk.num_stages) if (blocked[k] >> i) & 1] == case["infeasible"]
+            orders, off, ch = structure(case)
+            with pytest.raises(listsched.OrderInfeasible) as err:
+                listsched.run_order(inst, orders, off, ch)
+            assert list(err.value.stages) == case["infeasible"]
+            n += 1
+    assert n >= (20 if explicit else 150)

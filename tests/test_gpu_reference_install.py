@@ -140,3 +140,38 @@ def test_reference_online_sim_starts_from_the_gpu_search(cuda_ok, ps):
     cpu = ps.start_session(c1, budget, warm=winner)
     assert rep.solver_status == cpu.outcome.status
     assert spans[n_search:] == [e.makespan for e in ps.incumbent_stream(cpu)]
+
+
+def _ev(s):
+    if s is None:
+        return None
+    return ([(e.op.stage, e.op.microbatch, int(e.op.kind), e.start, e.end) for e in s.compute],
+            [(e.op.stage, e.op.microbatch, e.kind.value, e.start, e.end) for e in s.transfers])
+
+
+def test_radius_adapt_equals_reference_adapt_of_every_entry(cuda_ok, ps, tmp_path):
+    """cache.adapt_radius re-times every entry within the lookup radius in one launch; each result
+    equals the reference's own adapt of that entry (cache.py:224-240), and the best is at least as
+    good as the reference's single lookup hit (cache.py:243-259)."""
+    from test_integrate import _near_instances
+    from paper_2510_05186_b200.cache import adapt_radius, entry_from_record
+    insts = _near_instances(ps)
+    db = ps.CacheDb(tmp_path / "c.jsonl")
+    for inst in insts:
+        for s in (ps.sequential_schedule(inst), ps.best_feasible(inst, ps.AdaParams())[0]):
+            db.append(ps.entry_from_schedule(inst, s))
+    entries = db.entries()
+    records = [entry_from_record(e.to_dict()) for e in entries]
+    compared = 0
+    for inst in insts:
+        best, k, allr = adapt_radius(records, inst)
+        for idx, s in allr:
+            assert _ev(s) == _ev(ps.adapt(entries[idx], inst)), idx
+            compared += 1
+        hit = ps.lookup(db, ps.discretize(inst))
+        if hit is not None:
+            ref = ps.adapt(hit, inst)
+            if ref is not None:
+                from paper_2510_05186_b200 import makespan as our_makespan
+                assert best is not None and ps.makespan(ref, inst) >= our_makespan(best, inst)
+    assert compared >= len(insts)

@@ -355,3 +355,25 @@ def test_kernels_are_memcheck_clean(cuda_ok):
     r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "3", "--print-limit", "5",
                         sys.executable, "-c", script], capture_output=True, text=True, timeout=540)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_iterated_local_search_follows_the_cpu_restatement(cuda_ok):
+    """ILS: descents, kicks from the best, the same improvement trail and the same
+    best structure as the CPU restatement (tests/_search_cpu.py)."""
+    from _search_cpu import cpu_search
+    from oracle.oracle import Oracle
+    inst, orders, off, LocalSearch, SearchConfig = _setup(2)
+    n, kicks, km = 1024, 3, 4
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT, kick_moves=km))
+    orc = Oracle(ls.di.packed)
+    want = cpu_search(orc, ls.inc_orders.cpu().numpy().view(np.uint16), ls.inc_mask.cpu().numpy().view(np.uint32),
+                      SEED, PERMILLE, MAXSHIFT, n, kick_moves=km, kicks=kicks)
+    res = ls.run(kicks=kicks)
+    assert [(i.round, i.makespan, i.index) for i in res.improvements] == want["trail"]
+    assert (ls.round, ls.kicks) == (want["rounds"], want["kicks"])
+    assert res.makespan == want["best_span"] < ls.initial_makespan
+    assert (ls.best_orders.cpu().numpy().view(np.uint16) == want["best_orders"]).all()
+    assert (ls.best_mask.cpu().numpy().view(np.uint32) == want["best_mask"]).all()
+    from paper_2510_05186_b200 import makespan, validate
+    assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == res.makespan

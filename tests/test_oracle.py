@@ -53,12 +53,31 @@ def test_philox_known_answers():
         [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
 
 
-def test_malformed_candidates_are_flagged():
+def test_malformed_rows_follow_the_reference():
+    """Rows with a repeated op, a missing op, a cut tail or nothing at all: the reference replays
+    them literally and raises OrderInfeasible with the rows not yet exhausted
+    (tests/golden/malformed.json.gz, make_malformed_golden.py)."""
+    n = 0
+    for inst, pk, cases in corpus("malformed"):
+        orc = Oracle(pk)
+        for case in cases:
+            orders, mask, chans = case_arrays(pk, case)
+            r = orc.run(orders, mask, chans)
+            assert r["flags"] == 2, case["damage"]
+            assert [i + 1 for i in range(pk.num_stages) if (r["blocked"] >> i) & 1] == case["infeasible"], case["damage"]
+            n += 1
+    assert n >= 150
+
+
+def test_codes_naming_no_op_are_malformed():
     inst, pk, cases = corpus("ref_tests")[0]
     orc = Oracle(pk)
     orders, mask, _ = case_arrays(pk, cases[0])
     bad = orders.copy()
-    bad[0, 1] = bad[0, 0]          # duplicate op
+    bad[0, 1] = (pk.num_microbatches + 2) << 2     # microbatch out of range
+    assert orc.run(bad, mask)["flags"] == 4
+    bad = orders.copy()
+    bad[0, 1] = bad[0, 1] | 3                       # kind 3
     assert orc.run(bad, mask)["flags"] == 4
 
 
