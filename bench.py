@@ -276,6 +276,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttb", action="store_true")
     ap.add_argument("--ttb-rounds", type=int, default=1000)
+    ap.add_argument("--ils-seconds", type=float, default=10.0)
     # other BASELINE configs for manual runs (the driver's line is config 3, 65,536 per GPU)
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--per-gpu", type=int, default=65536)
@@ -323,11 +324,17 @@ def main():
                             ls.count, ls.moves, events_total.data_ptr(),
                             ls.base.handle if ls.base is not None else None)
         ev_k0.record(stream)
-        N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()), None,
-                                    C.c_void_p(stream.cuda_stream)))
-        ev_k1.record(stream)
-        if world > 1:
-            dist.all_reduce(ls.best_key, op=dist.ReduceOp.MIN)
+        if ls.nccl_comm:
+            # over NCCL the 8-byte all-reduce(MIN) runs inside the C ABI call, after the kernels
+            N.check(lib.ps_search_round_sharded(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()), None,
+                                                C.c_void_p(ls.nccl_comm), C.c_void_p(stream.cuda_stream)))
+            ev_k1.record(stream)
+        else:
+            N.check(lib.ps_search_round(di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()), None,
+                                        C.c_void_p(stream.cuda_stream)))
+            ev_k1.record(stream)
+            if world > 1:
+                dist.all_reduce(ls.best_key, op=dist.ReduceOp.MIN)
         return ls.finish_round()
 
     # ---- warm-up -------------------------------------------------------------------------------
@@ -556,6 +563,22 @@ def main():
             ttb["distinct_move_fraction"] = frac
             ttb["cpu_port_seconds_to_best_estimate_dedup"] = ttb["cpu_port_seconds_to_best_estimate"] * frac
         line["time_to_best"] = ttb
+        # the iterated local search past the descent's convergence, same warm start
+        cfg_ils = SearchConfig(seed=SEED, neighbours=PER_GPU * world, kick_moves=4, **MOVES)
+        ls4 = LocalSearch(inst, orders0, s0.offloaded, cfg_ils, device=local)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        res4 = ls4.run(time_budget=args.ils_seconds)
+        marks = [t for t in (0.5, 1.0, 2.0, 5.0, 10.0, 30.0) if t <= args.ils_seconds]
+        at = {str(t): min([ls4.initial_makespan] + [i.makespan for i in res4.improvements if i.timestamp <= t])
+              for t in marks}
+        line["time_to_best_ils"] = {"seconds": args.ils_seconds, "best_makespan": res4.makespan,
+                                    "best_at_seconds": at, "rounds": ls4.round, "kicks": ls4.kicks,
+                                    "kick_moves": 4, "improvement_pct": 100.0 * (ls4.initial_makespan - res4.makespan)
+                                    / ls4.initial_makespan,
+                                    "note": "descent + kicks from the best (DESIGN.md 4.1) for a fixed wall-clock "
+                                            "budget; the descent alone stops at its local optimum (time_to_best)"}
     # ---- whole search without deduplication: every neighbour of every round simulated, rounds from
     # the warm start to convergence (the early rounds of `value` are the cheapest ones) ------------
     if not args.no_ttb:

@@ -5,6 +5,8 @@
 Per config:
 * gpu        LocalSearch from the best_feasible warm start (BASELINE's neighbours per round),
              until 16 rounds bring nothing: every strict improvement with its wall-clock time.
+* gpu_ils    the iterated local search (kicks from the best) for the same
+             wall-clock budget as the reference solver.
 * cpu_port   the IDENTICAL search on the host cores: the C restatement of run_order evaluates
              every neighbour of every round (oracle/ps_oracle.c or_search_round, all threads),
              the same (makespan, index) selection, the same move applied — its improvement trail
@@ -66,6 +68,25 @@ def gpu_arm(inst, cfg):
     return {"warm_start": name, "warm_seconds": t_warm, "search_seconds": elapsed, "rounds": ls.round,
             "neighbours_per_round": sc.neighbours, "stream": stream,
             "trail": [[imp.round, imp.makespan, imp.index] for imp in ls.improvements]}, ls, s0
+
+
+def gpu_ils_arm(inst, cfg, budget, kick_moves=4):
+    """Iterated local search for `budget` seconds from the same warm start."""
+    import torch
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+    t0 = time.perf_counter()
+    s0, name = best_feasible(inst, device=0)
+    t_warm = time.perf_counter() - t0
+    orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
+    sc = SearchConfig(seed=SEED, neighbours=NEIGHBOURS[cfg], kick_moves=kick_moves, **MOVES)
+    ls = LocalSearch(inst, orders, s0.offloaded, sc, device=0)
+    res = ls.run(time_budget=budget - t_warm)
+    stream = [(t_warm, ls.initial_makespan)] + [(t_warm + imp.timestamp, imp.makespan) for imp in res.improvements]
+    return {"warm_start": name, "warm_seconds": t_warm, "budget_seconds": budget, "rounds": ls.round,
+            "kicks": ls.kicks, "kick_moves": kick_moves, "neighbours_per_round": sc.neighbours,
+            "stream": stream}, res.schedule
 
 
 def cpu_port_arm(inst, cfg, s0, max_rounds, max_seconds):
@@ -141,10 +162,16 @@ def main():
         res["cpu_model"] = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
     except Exception:
         pass
+    # CUDA context, library load and first-launch costs are paid once per process, not per search
+    import torch
+    from paper_2510_05186_b200.heuristics import best_feasible
+    best_feasible(workloads.config1(), device=0)
+    torch.cuda.synchronize()
     for cfg in args.configs:
         inst = workloads.CONFIGS[cfg]()
         row = {}
         row["gpu"], ls, s0 = gpu_arm(inst, cfg)
+        row["gpu_ils"], _ = gpu_ils_arm(inst, cfg, REF_BUDGET[cfg])
         cap = args.cpu_rounds if cfg == 3 else 5000
         row["cpu_port"] = cpu_port_arm(inst, cfg, s0, cap, 900.0)
         k = len(row["cpu_port"]["trail"])
@@ -157,7 +184,7 @@ def main():
             row["cpu_port"]["seconds_to_gpu_best_projected"] = per * last
         row["reference_bnb"] = ref_arm(inst, cfg) if cfg in (1, 2) else {"skipped": "BASELINE.md §2 plans the B&B stream for configs 1 and 2"}
         row["best_at"] = {str(t): {arm: best_at(row[arm]["stream"], t) if "stream" in row[arm] else None
-                                   for arm in ("gpu", "cpu_port", "reference_bnb")} for t in MARKS}
+                                   for arm in ("gpu", "gpu_ils", "cpu_port", "reference_bnb")} for t in MARKS}
         res["configs"][str(cfg)] = row
         print(json.dumps({cfg: row["best_at"]}), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
