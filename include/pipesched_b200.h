@@ -9,6 +9,7 @@
  *                      and the bubble ratio                     (cli.py:115, 156),
  *                      for a whole batch of candidate structures at once.
  *   ps_eval_batch_host the same call on HOST buffers (copies in and out inside the call).
+ *   ps_search_round_sharded  the same over G ranks: + one 8-byte NCCL all-reduce(MIN) per round
  *   ps_search_round    neighbour generation + evaluation + best-of selection of one local-search
  *                      round (no reference counterpart: SURVEY.md §0 "Not in the reference");
  *                      its result feeds solver.start_session(warm=...) (solver.py:543-565).
@@ -49,7 +50,13 @@ extern "C" {
 
 #define PS_FLAG_FEASIBLE 1u     /* complete schedule; STRICT peak <= limit by construction */
 #define PS_FLAG_DEADLOCK 2u     /* no event can start: the reference raises OrderInfeasible */
-#define PS_FLAG_MALFORMED 4u    /* stage order is not a permutation / bad channel order    */
+#define PS_FLAG_MALFORMED 4u    /* an op code names no op of its stage / bad offload bit / bad channel order */
+#define PS_FLAG_RANGE 16u       /* an event time of this candidate reached 2^29 quanta (not evaluated)   */
+
+/* Stage rows: 3m op codes (microbatch << 2 | kind), or fewer ending with PS_ROW_END (0xFFFF;
+   0xFF for uint8 codes).  A row that repeats an op or is short is replayed literally, as the
+   reference does (listsched.py:206-252): it ends in PS_FLAG_DEADLOCK with the blocked stages. */
+#define PS_ROW_END 0xFFFFu
 
 #define PS_MAX_STAGES 32
 #define PS_MAX_MICROBATCHES 4096
@@ -189,6 +196,17 @@ int ps_eval_batch_host(const ps_instance *inst, const ps_cand_batch *batch,
    makespan_out (device int64 [count], optional) receives every neighbour's makespan or -1. */
 int ps_search_round(const ps_instance *inst, const ps_search_desc *desc,
                     int64_t *best_key, int64_t *makespan_out, void *stream);
+
+/* The round of a search sharded over G ranks (one process per GPU): each rank
+   passes its contiguous shard [first_index, first_index + count) of the round's global neighbour
+   indices; after the local round the 8-byte key is combined across ranks with one
+   ncclAllReduce(MIN) on `stream`, so every rank holds the round's global best key on return (the
+   lowest global index wins ties, so the winner is the same for every G).  nccl_comm is an
+   ncclComm_t owned by the caller (NULL = a single rank: the same as ps_search_round).
+   libnccl.so.2 is loaded on first use (the library does not link against it).  Replaces the
+   reference's sequential selection loop (heuristics.py:206; solver.py:437) for one round. */
+int ps_search_round_sharded(const ps_instance *inst, const ps_search_desc *desc,
+                            int64_t *best_key, int64_t *makespan_out, void *nccl_comm, void *stream);
 
 /* Materialise neighbours [first_index, first_index+count) as full candidates (device buffers
    shaped like ps_cand_batch: orders [count][P][order_stride], masks [count][mask_words]). */

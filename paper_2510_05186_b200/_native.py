@@ -18,6 +18,7 @@ PS_OK = 0
 FLAG_FEASIBLE = 1
 FLAG_DEADLOCK = 2
 FLAG_MALFORMED = 4
+FLAG_RANGE = 16          # an event time reached 2^29 quanta (include/pipesched_b200.h)
 MAX_STAGES = 32
 MAX_MICROBATCHES = 4096
 BEST_NONE = (1 << 63) - 1
@@ -133,6 +134,8 @@ EXPORTS = {
     "ps_eval_batch": (C.c_int, [C.c_void_p, C.POINTER(CandBatch), C.POINTER(ResultBatch), C.c_void_p]),
     "ps_eval_batch_host": (C.c_int, [C.c_void_p, C.POINTER(CandBatch), C.POINTER(ResultBatch), C.c_void_p]),
     "ps_search_round": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_search_round_sharded": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p]),
     "ps_materialize_moves": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
     "ps_apply_move": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(MoveParams),
                                 C.c_uint64, C.c_uint64, C.c_void_p]),

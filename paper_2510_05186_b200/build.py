@@ -69,7 +69,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: Path | No
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = lib.with_suffix(".so.tmp")
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)])
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs), "-ldl"])
     os.replace(tmp, lib)
     return lib
 

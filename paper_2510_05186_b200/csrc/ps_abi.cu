@@ -1,5 +1,7 @@
 // ps_abi.cu — C ABI (include/pipesched_b200.h): instance tables, launch planning, search kernels.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <stdarg.h>
@@ -26,6 +28,7 @@ struct ps_instance {
     int max_smem_optin;
     int P, m, G, L, MW, stride, mask_words;
     int comm, toff, post, uniform, any_off;
+    int time_safe;            // see EvalParams::time_safe
     int64_t busy, unit;
     bool v64;
     int32_t *d_proc;
@@ -250,7 +253,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
 void fill_instance(const ps_instance *I, EvalParams *p) {
     p->P = I->P; p->m = I->m; p->G = I->G; p->L = I->L; p->MW = I->MW; p->stride = I->stride;
     p->comm = I->comm; p->toff = I->toff; p->post = I->post; p->uniform = I->uniform;
-    p->any_off = I->any_off; p->busy = I->busy; p->unit = I->unit;
+    p->any_off = I->any_off; p->busy = I->busy; p->unit = I->unit; p->time_safe = I->time_safe;
     p->proc = I->d_proc; p->vals = I->d_vals; p->limit = I->d_limit; p->chan = I->d_chan;
 }
 
@@ -640,10 +643,17 @@ int ps_instance_create(const ps_instance_desc *d, int device, ps_instance **out)
             }
         }
     }
-    // every event time must stay below 2^29 (times are packed as (t << 2 | state) in 32 bits)
+    // Event times are packed as (t << 2 | state) in 32 bits, so every event must end below 2^29.
+    // Durations must fit well inside that; the instance's horizon (no event of any structure can
+    // end later) decides whether the kernels check at all: past it, an event chosen to start at or
+    // after 2^29 - (longest duration) ends that candidate with PS_FLAG_RANGE (ps_eval.cuh), so
+    // instances with long horizons are accepted and every schedule whose times fit is exact.
+    int64_t max_dur = std::max<int64_t>(d->comm_time, d->offload_time);
+    for (size_t k = 0; k < (size_t)P * m * 3; ++k) max_dur = std::max<int64_t>(max_dur, d->proc_time[k]);
+    if (max_dur >= (int64_t)1 << 27)
+        return fail(PS_ERR_RANGE, "a duration of %lld quanta exceeds the 2^27 range", (long long)max_dur);
     double horizon = (double)busy + 2.0 * n_off * d->offload_time + (2.0 * m * P + 1.0) * d->comm_time;
-    if (horizon >= (double)(1 << 29))
-        return fail(PS_ERR_RANGE, "instance horizon %.0f quanta exceeds the 2^29 time range", horizon);
+    const int time_safe = horizon < (double)(1 << 29) ? INT_MAX : (int)((1 << 29) - max_dur);
     // ledger width: usage never exceeds the sum of a stage's F deltas
     bool v64 = false;
     for (int i = 0; i < P; ++i) {
@@ -660,6 +670,7 @@ int ps_instance_create(const ps_instance_desc *d, int device, ps_instance **out)
     I->mask_words = (P * m + 31) / 32;
     I->comm = (int)d->comm_time; I->toff = (int)d->offload_time; I->post = d->post_validation != 0;
     I->uniform = uniform; I->any_off = any_off; I->busy = busy; I->unit = unit; I->v64 = v64;
+    I->time_safe = time_safe;
     I->h_offloadable.resize((size_t)P * m);
     for (size_t k = 0; k < (size_t)P * m; ++k) I->h_offloadable[k] = d->act_size[k] > 0;
 
@@ -1113,6 +1124,42 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.dedup = makespan_out == nullptr && d->dedup;
     p.events_total = (unsigned long long *)d->events_total;
     return run_eval(I, p, true, (cudaStream_t)stream, d->base);
+}
+
+// NCCL, resolved at run time: the library stays loadable on hosts without NCCL, and shares the
+// process's libnccl.so.2 (e.g. the one torch.distributed already loaded) with the caller.
+typedef ncclResult_t (*AllReduceFn)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                    cudaStream_t);
+typedef const char *(*ErrStrFn)(ncclResult_t);
+static AllReduceFn nccl_allreduce(ErrStrFn *errstr) {
+    static AllReduceFn fn = nullptr;
+    static ErrStrFn es = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            fn = (AllReduceFn)dlsym(h, "ncclAllReduce");
+            es = (ErrStrFn)dlsym(h, "ncclGetErrorString");
+        }
+    });
+    if (errstr) *errstr = es;
+    return fn;
+}
+
+int ps_search_round_sharded(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
+                            void *nccl_comm, void *stream) {
+    int rc = ps_search_round(I, d, best_key, makespan_out, stream);
+    if (rc || !nccl_comm) return rc;
+    ErrStrFn es = nullptr;
+    AllReduceFn ar = nccl_allreduce(&es);
+    if (!ar) return fail(PS_ERR_INVALID, "libnccl.so.2 not found: cannot combine the round across ranks");
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    ncclResult_t r = ar(best_key, best_key, 1, ncclInt64, ncclMin, (ncclComm_t)nccl_comm, (cudaStream_t)stream);
+    if (r != ncclSuccess) return fail(PS_ERR_CUDA, "ncclAllReduce: %s", es ? es(r) : "error");
+    return PS_OK;
 }
 
 int ps_materialize_moves(const ps_instance *I, const ps_search_desc *d, uint16_t *orders_out, uint32_t *mask_out,

@@ -30,7 +30,8 @@
 
 namespace ps {
 
-constexpr uint32_t FLAG_FEASIBLE = 1u, FLAG_DEADLOCK = 2u, FLAG_MALFORMED = 4u, FLAG_OVERFLOW = 8u;
+constexpr uint32_t FLAG_FEASIBLE = 1u, FLAG_DEADLOCK = 2u, FLAG_MALFORMED = 4u, FLAG_OVERFLOW = 8u,
+                   FLAG_RANGE = 16u;   // an event time reached 2^29 quanta (see EvalParams::time_safe)
 constexpr int TAU_NONE = INT_MAX;   // usage never drops far enough: earliest_fit returns None
 constexpr int TAU_ANY = INT_MIN;    // fits at any query time at or above the fold line
 constexpr uint32_t NO_CHAN = 0xFFFFFFFFu;
@@ -39,6 +40,10 @@ struct EvalParams {
     // instance (device tables)
     int P, m, G, L, MW, stride;
     int comm, toff, post, uniform, any_off;
+    // Times are packed as (t << 2 | state) in 32 bits, so every event must END below 2^29: an event
+    // chosen to start at or after time_safe = 2^29 - (longest duration) ends the candidate with
+    // FLAG_RANGE.  INT_MAX when no schedule of the instance can get there (its horizon bound).
+    int time_safe;
     int64_t busy, unit;
     const int32_t *proc;     // [rows][3]
     const void *vals;        // V [rows][4] = dF, dB, dW, gamma (in memory units)
@@ -1051,6 +1056,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         int max_win = REC && cc0 > 0 ? (int)p.ck[(size_t)(cc0 / p.ck_interval) * p.ck_words + ck_r + 9] : 0;
         int conv_c = -1;
         bool early_dl = false;
+        bool range_ovf = false;
         for (;;) {
             if (REC) max_win = max(max_win, __reduce_max_sync(0xffffffffu, we - ws));
             if (cdirty) { compute_key(); cdirty = false; }
@@ -1072,6 +1078,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             if (mh == KEY_NONE) break;
 
             const int t = (int)mh;
+            if (t >= p.time_safe) { range_ovf = true; break; }     // (warp-uniform)
             const int rank = (int)(ml >> 30);
             if (rank == RANK_COMPUTE && (cc & (p.ck_interval - 1)) == 0) {
                 const int c = cc / p.ck_interval;
@@ -1288,9 +1295,15 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             __syncwarp();
             continue;
         }
+        if (!REC && range_ovf) {
+            if (lane == 0) put_result(FLAG_RANGE, -1LL, 0u, 0);
+            if (p.peak && has_stage) p.peak[(size_t)cand * P + i] = -1;
+            __syncwarp();
+            continue;
+        }
         const unsigned rem = __ballot_sync(0xffffffffu, has_stage && pos < L);
         if (REC) {
-            const bool unusable = __any_sync(0xffffffffu, ovf || ck_full);
+            const bool unusable = __any_sync(0xffffffffu, ovf || ck_full) || range_ovf;
             long long span = -1;
             if (!unusable && rem == 0u) {
                 win_fold(INT_MAX);
@@ -1324,7 +1337,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 p.base_info[5] = -1;                      // no shifted suffix to apply
                 p.base_info[0] = unusable || cc == 0 ? -1 : (cc - 1) / p.ck_interval + 1;
                 p.base_info[4] = max_win;
-                p.base_info[1] = (int)(rem == 0u ? FLAG_FEASIBLE : FLAG_DEADLOCK);
+                p.base_info[1] = (int)(rem == 0u ? FLAG_FEASIBLE : range_ovf ? FLAG_RANGE : FLAG_DEADLOCK);
                 p.base_info[2] = ecount;
                 p.base_info[3] = (int)rem;
                 p.base_res[0] = span;

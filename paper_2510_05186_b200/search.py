@@ -94,6 +94,25 @@ def combine_keys(key_tensor, group=None):
     return key_tensor
 
 
+def nccl_comm_ptr(group=None, device=None) -> int | None:
+    """The ncclComm_t behind a torch.distributed NCCL process group (created on first use), for
+    ps_search_round_sharded; None for other backends or when torch does not expose it."""
+    import torch
+    import torch.distributed as dist
+    try:
+        if dist.get_backend(group) != "nccl":
+            return None
+        pg = group if group is not None else dist.distributed_c10d._get_default_group()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        warm = torch.zeros(1, dtype=torch.int64, device=dev)
+        dist.all_reduce(warm, group=group)          # the communicator exists after a first collective
+        torch.cuda.synchronize(dev)
+        ptr = int(pg._get_backend(dev)._comm_ptr())
+        return ptr or None
+    except Exception:
+        return None
+
+
 def agree_stop(stop: bool, device, group=None) -> bool:
     """The ranks' joint stop decision: stop when ANY rank wants to.  Wall-clock budgets are read
     on each rank's own clock, so without this one rank could leave the loop while another enters
@@ -134,6 +153,10 @@ class LocalSearch:
         self.rank = dist.get_rank(group) if self.distributed else 0
         self.world = dist.get_world_size(group) if self.distributed else 1
         self.first, self.count = shard_range(config.neighbours, self.rank, self.world)
+        # over NCCL the round's 8-byte all-reduce(MIN) runs inside the C ABI call
+        # (ps_search_round_sharded) on the torch group's communicator; other backends combine
+        # the key with torch.distributed
+        self.nccl_comm = nccl_comm_ptr(group, self.di.device) if self.world > 1 else None
         self.moves = N.MoveParams(config.seed & (2**64 - 1), config.shift_permille, config.max_shift)
         res = self.di.evaluate(self.inc_orders.view(1, *self.inc_orders.shape),
                                self.inc_mask.view(1, -1), peak=False)
@@ -167,9 +190,13 @@ class LocalSearch:
         desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round,
                             self.first, self.count, self.moves, None,
                             self.base.handle if self.base is not None else None, int(self.cfg.dedup))
+        ms = C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None
+        if self.nccl_comm:
+            N.check(self.lib.ps_search_round_sharded(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
+                                                     ms, C.c_void_p(self.nccl_comm), self._stream()))
+            return
         N.check(self.lib.ps_search_round(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
-                                         C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None,
-                                         self._stream()))
+                                         ms, self._stream()))
         if self.world > 1:
             combine_keys(self.best_key, self.group)
 
