@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <stdarg.h>
@@ -21,6 +22,20 @@
 #include "ps_literal.h"
 
 using namespace ps;
+
+namespace {
+// NVTX ranges around every entry point (header-only NVTX3: free unless a profiler is attached),
+// so nsys/ncu timelines show rounds, batches and recordings by name.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    NvtxRange(const char *fmt, unsigned long long v) {
+        char buf[96];
+        snprintf(buf, sizeof buf, fmt, v);
+        nvtxRangePushA(buf);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct ps_instance {
     int device;
@@ -119,6 +134,7 @@ struct Plan {
     int K, warps;
     bool gstate;
     int cand_words, inc_words;
+    int dirty_words = 0;
     LaunchCfg cfg;
     size_t scratch_bytes;
 };
@@ -221,7 +237,9 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
         pl->gstate = true;
         pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
-        pl->cfg.smem = (size_t)pl->inc_words * 4;
+        // (move mode) each warp's dirty bitmap of its slot's end-time words (ps_eval.cuh TRACK)
+        pl->dirty_words = moves && env_int("PS_GSTATE_TRACK", 1) ? (((2 * I->P * I->m + 31) / 32 + 3) & ~3) : 0;
+        pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * pl->dirty_words) * 4;
         pl->cfg.block = 32 * pl->warps;
     };
     int per_sm = 0, rc;
@@ -324,6 +342,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.K = pl.K;
         q.cand_words = pl.cand_words;
         q.inc_words = pl.inc_words;
+        q.dirty_words = pl.gstate ? pl.dirty_words : 0;
         int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order;         // handoff k-1
         int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
         q.work_count = in;
@@ -815,6 +834,7 @@ int ps_base_destroy(ps_base *B) {
 }
 
 int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, void *stream) {
+    NvtxRange nvtx("ps_base_record");
     if (!B || !orders || !mask) return fail(PS_ERR_INVALID, "null argument");
     const ps_instance *I = B->inst;
     DeviceGuard guard(I->device);
@@ -918,6 +938,7 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
                            cudaStream_t stream, const int32_t *ready, int64_t ready_chunk);
 
 int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
+    NvtxRange nvtx("ps_eval_batch n=%llu", (unsigned long long)(b ? b->num_candidates : 0));
     return eval_batch_impl(I, b, r, (cudaStream_t)stream, nullptr, 0);
 }
 
@@ -986,6 +1007,7 @@ static const int32_t *pinned_one() {
 }
 
 int ps_eval_batch_host(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
+    NvtxRange nvtx("ps_eval_batch_host n=%llu", (unsigned long long)(b ? b->num_candidates : 0));
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
     const int64_t N = b->num_candidates;
     if (N <= 0) return N == 0 ? PS_OK : fail(PS_ERR_INVALID, "negative candidate count");
@@ -1085,6 +1107,7 @@ extern "C" cudaError_t ps_bound_launch(int P, int m, int uniform, int post, int 
                             int num_sms, cudaStream_t s);
 
 int ps_bound_batch_eval(const ps_instance *I, const ps_bound_batch *b, int64_t *lower_bound, void *stream) {
+    NvtxRange nvtx("ps_bound_batch_eval");
     if (!I || !b || !lower_bound) return fail(PS_ERR_INVALID, "null argument");
     if (b->num_nodes < 0) return fail(PS_ERR_INVALID, "negative node count");
     if (b->num_nodes == 0) return PS_OK;
@@ -1099,6 +1122,7 @@ int ps_bound_batch_eval(const ps_instance *I, const ps_bound_batch *b, int64_t *
 
 int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
                     void *stream) {
+    NvtxRange nvtx("ps_search_round r=%llu", (unsigned long long)(d ? d->round : 0));
     if (!I || !d || !best_key) return fail(PS_ERR_INVALID, "null argument");
     if (!d->inc_orders || !d->inc_mask) return fail(PS_ERR_INVALID, "incumbent buffers are required");
     if (d->count < 0 || d->first_index < 0) return fail(PS_ERR_INVALID, "negative shard range");
@@ -1150,6 +1174,7 @@ static AllReduceFn nccl_allreduce(ErrStrFn *errstr) {
 
 int ps_search_round_sharded(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
                             void *nccl_comm, void *stream) {
+    NvtxRange nvtx("ps_search_round_sharded");
     int rc = ps_search_round(I, d, best_key, makespan_out, stream);
     if (rc || !nccl_comm) return rc;
     ErrStrFn es = nullptr;
@@ -1178,6 +1203,7 @@ int ps_materialize_moves(const ps_instance *I, const ps_search_desc *d, uint16_t
 
 int ps_apply_move(const ps_instance *I, uint16_t *inc_orders, uint32_t *inc_mask, const ps_move_params *mp,
                   uint64_t round, uint64_t index, void *stream) {
+    NvtxRange nvtx("ps_apply_move");
     if (!I || !inc_orders || !inc_mask || !mp) return fail(PS_ERR_INVALID, "null argument");
     DeviceGuard guard(I->device);
     if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);

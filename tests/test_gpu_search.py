@@ -324,10 +324,35 @@ def test_search_resumes_from_a_checkpoint(cuda_ok):
     assert (resumed.inc_orders.cpu() == full.inc_orders.cpu()).all()
 
 
-@pytest.mark.timeout(600)
-def test_kernels_are_memcheck_clean(cuda_ok):
-    """compute-sanitizer memcheck over a recording, a bounded search, a host-buffer batch and the
-    node bounds (sanitizers on the GPU box)."""
+SANITIZER_SCRIPT = (
+    "import sys; sys.path.insert(0, %r)\n"
+    "import numpy as np, torch\n"
+    "from paper_2510_05186_b200 import workloads\n"
+    "from paper_2510_05186_b200.heuristics import best_feasible\n"
+    "from paper_2510_05186_b200.listsched import stage_order_of\n"
+    "from paper_2510_05186_b200.search import LocalSearch, SearchConfig\n"
+    "from paper_2510_05186_b200.bound import lower_bounds\n"
+    "inst = workloads.CONFIGS[2]()\n"
+    "s, _ = best_feasible(inst)\n"
+    "o = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}\n"
+    "ls = LocalSearch(inst, o, s.offloaded, SearchConfig(seed=1, neighbours=512, kick_moves=2))\n"
+    "ls.run(rounds=3)\n"
+    "ls.kick()\n"
+    "ls.run(rounds=5)\n"
+    "od, md = ls.materialize(0, 256)\n"
+    "ho = od.cpu().numpy().view(np.uint16).copy()\n"
+    "ho[1, 0, 1] = ho[1, 0, 0]\n"                 # a repeated op: the literal replay pass
+    "ls.di.evaluate_host(ho.astype(np.uint8), md.cpu().numpy(), base=ls.base)\n"
+    "print(lower_bounds(inst, [(0, {i: 0 for i in range(1, inst.num_stages + 1)}, {})]))\n"
+)
+
+
+@pytest.mark.timeout(1200)
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_kernels_are_sanitizer_clean(cuda_ok, tool):
+    """compute-sanitizer memcheck / synccheck over a recording, bounded search rounds, an ILS kick,
+    a host-buffer batch with a malformed row (the literal replay kernel) and the node bounds
+    (sanitizers on the GPU box)."""
     import os
     import shutil
     import subprocess
@@ -335,25 +360,9 @@ def test_kernels_are_memcheck_clean(cuda_ok):
     san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(san):
         pytest.skip("compute-sanitizer not installed")
-    script = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import numpy as np, torch\n"
-        "from paper_2510_05186_b200 import workloads\n"
-        "from paper_2510_05186_b200.heuristics import best_feasible\n"
-        "from paper_2510_05186_b200.listsched import stage_order_of\n"
-        "from paper_2510_05186_b200.search import LocalSearch, SearchConfig\n"
-        "from paper_2510_05186_b200.bound import lower_bounds\n"
-        "inst = workloads.CONFIGS[2]()\n"
-        "s, _ = best_feasible(inst)\n"
-        "o = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}\n"
-        "ls = LocalSearch(inst, o, s.offloaded, SearchConfig(seed=1, neighbours=512))\n"
-        "ls.run(rounds=3)\n"
-        "od, md = ls.materialize(0, 256)\n"
-        "ls.di.evaluate_host(od.cpu().numpy().astype(np.uint8), md.cpu().numpy(), base=ls.base)\n"
-        "print(lower_bounds(inst, [(0, {i: 0 for i in range(1, inst.num_stages + 1)}, {})]))\n"
-    ) % str(Path(__file__).resolve().parents[1])
-    r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "3", "--print-limit", "5",
-                        sys.executable, "-c", script], capture_output=True, text=True, timeout=540)
+    script = SANITIZER_SCRIPT % str(Path(__file__).resolve().parents[1])
+    r = subprocess.run([san, "--tool", tool, "--error-exitcode", "3", "--print-limit", "5",
+                        sys.executable, "-c", script], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
