@@ -15,8 +15,11 @@ Keys beyond the driver contract:
   cpu_baseline  the C restatement of the reference algorithm (oracle/, "port"), all host
                 threads, on the first neighbours of the same round; parity of that sample
                 with the GPU is checked and reported.
-  e2e           the same metric through ps_eval_batch_host: materialised candidates in
-                pinned host memory, copied in, evaluated, results copied out, every step.
+  e2e           the same metric through the C ABI with HOST buffers: the round's neighbours as
+                differences from the incumbent (ps_eval_batch_host_delta) in pinned host memory,
+                copied in, rebuilt and evaluated with the incumbent as base, results copied out,
+                every step; e2e_rows the same with full stage rows (ps_eval_batch_host), and
+                e2e_no_base full rows with no base (every candidate simulated in full).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -396,7 +399,8 @@ def main():
     # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the committed ncu --set full
     # capture of the same command (ncu cannot run inside the timed bench)
     traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", "ncu_eval_summary.json")
+    prof = os.path.join(ROOT, "profiles", {3: "ncu_eval_summary.json", 5: "ncu_eval_config5_summary.json"}.get(
+        CONFIG, "ncu_eval_config%d_summary.json" % CONFIG))
     if os.path.exists(prof):
         try:
             doc = json.load(open(prof))
@@ -467,12 +471,49 @@ def main():
         if world > 1:
             dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
         e_s = float(e_tot.item()) / 1e3
-        line["e2e"] = {"value": n_cand * world * K / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * e_s / K,
-                       "api": "ps_eval_batch_host (pinned host buffers, copies inside the call)",
-                       "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate"}
+        line["e2e_rows"] = {"value": n_cand * world * K / e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                            "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * e_s / K,
+                            "api": "ps_eval_batch_host (full stage rows, uint8 codes when m <= 64; pinned host "
+                                   "buffers, copies inside the call)",
+                            "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate"}
         e2e_flags = outs["flags"].numpy().copy()
         e2e_span = outs["makespan"].numpy().copy()
+        # the headline e2e: the same neighbours in the compact host form, differences from the
+        # incumbent (ps_delta_batch: only those cross PCIe; rebuilt in HBM by a kernel)
+        from paper_2510_05186_b200.packing import delta_encode
+        ref_o = ls.inc_orders.cpu().numpy().view(np.uint16).copy()
+        ref_m = ls.inc_mask.cpu().numpy().view(np.uint32).copy()
+        enc = delta_encode(ref_o, ref_m, orders_d.cpu().numpy().view(np.uint16), masks_d.cpu().numpy().view(np.uint32))
+        pinned = []
+        for a in (ref_o, ref_m) + tuple(enc):
+            t = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+            t.numpy()[:] = np.ascontiguousarray(a).view(np.uint8).ravel()
+            pinned.append(t)
+        db = N.DeltaBatch(n_cand, *[t.data_ptr() for t in pinned], ls.base.handle if ls.base is not None else None)
+        h2d_d = sum(t.numel() for t in pinned)
+        for _ in range(args.warmup):
+            N.check(lib.ps_eval_batch_host_delta(di.handle, C.byref(db), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+        if world > 1:
+            dist.barrier()
+        d_ms = []
+        for k in range(K):
+            flush.fill_(k & 0xFF)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            N.check(lib.ps_eval_batch_host_delta(di.handle, C.byref(db), C.byref(rb), C.c_void_p(stream.cuda_stream)))
+            d_ms.append(1000 * (time.perf_counter() - t0))
+        d_tot = torch.tensor([sum(d_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(d_tot, op=dist.ReduceOp.MAX)
+        d_s = float(d_tot.item()) / 1e3
+        same_d = bool((outs["makespan"].numpy() == e2e_span).all() and (outs["flags"].numpy() == e2e_flags).all())
+        line["e2e"] = {"value": n_cand * world * K / d_s, "unit": UNIT, "h2d_bytes_per_step": h2d_d,
+                       "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * d_s / K,
+                       "api": "ps_eval_batch_host_delta: pinned host buffers holding the neighbours as differences "
+                              "from the incumbent (ps_delta_batch), copied in, rebuilt and evaluated on the device "
+                              "with the incumbent as the recorded base, results copied out, every step",
+                       "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate",
+                       "outputs_equal_to_e2e_rows": same_d}
         # the same batch as a generic one: no recorded base, every candidate simulated from its
         # first event, like the CPU port (the like-for-like ratio against cpu_baseline)
         cb0 = N.CandBatch(n_cand, h_orders.data_ptr(), h_masks.data_ptr(), None, 0, None, 1 if u8 else 2)
@@ -493,9 +534,9 @@ def main():
                                "steps": k0, "ms_per_step": float(n_tot.item()) / k0,
                                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                                "outputs_equal_to_e2e": same,
-                               "note": "ps_eval_batch_host without a recorded base: no prefix/suffix sharing, "
-                                       "each candidate simulated in full (like the CPU port); e2e above resumes "
-                                       "from the incumbent's checkpoints"}
+                               "note": "ps_eval_batch_host on full rows without a recorded base: no prefix/suffix "
+                                       "sharing, each candidate simulated in full (like the CPU port); e2e and "
+                                       "e2e_rows resume from the incumbent's checkpoints"}
     else:
         line["e2e"] = None
 
@@ -542,9 +583,14 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         stale = 0
+        r_ms = []
         while ls2.round < args.ttb_rounds and stale < 16:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             ls2.launch_round()
+            e1.record(stream)
             stale = 0 if ls2.finish_round(t0) else stale + 1
+            r_ms.append(e0.elapsed_time(e1))
         elapsed = time.perf_counter() - t0
         last = ls2.improvements[-1] if ls2.improvements else None
         ttb = {"initial_makespan": ls2.initial_makespan, "best_makespan": ls2.makespan,
@@ -554,8 +600,10 @@ def main():
                "seconds_to_best": last.timestamp if last else 0.0, "search_seconds": elapsed,
                "stopped_by": "16 rounds without improvement" if stale >= 16 else f"round cap {args.ttb_rounds}",
                "neighbours_per_round": cfg.neighbours,
+               "ms_per_round_mean": sum(r_ms) / len(r_ms), "ms_per_round_last50": sum(r_ms[-50:]) / len(r_ms[-50:]),
                "note": "LocalSearch as shipped: a move drawn several times in a round is simulated once "
-                       "(lowest index); the trajectory is that of evaluating every neighbour"}
+                       "(lowest index) and a neighbour whose makespan bound reaches the incumbent's is "
+                       "abandoned (DESIGN.md 3.13); the trajectory is that of evaluating every neighbour"}
         if "cpu_baseline" in line:
             ttb["cpu_port_seconds_to_best_estimate"] = ttb["rounds_to_best"] * cfg.neighbours / line["cpu_baseline"]["value"]
             # the same search on the CPU with the same deduplication of repeated moves
@@ -582,7 +630,7 @@ def main():
     # ---- whole search without deduplication: every neighbour of every round simulated, rounds from
     # the warm start to convergence (the early rounds of `value` are the cheapest ones) ------------
     if not args.no_ttb:
-        cfg_nd = SearchConfig(seed=SEED, neighbours=PER_GPU * world, dedup=False, **MOVES)
+        cfg_nd = SearchConfig(seed=SEED, neighbours=PER_GPU * world, dedup=False, prune=False, **MOVES)
         ls3 = LocalSearch(inst, orders0, s0.offloaded, cfg_nd, device=local)
         torch.cuda.synchronize()
         if world > 1:

@@ -110,6 +110,23 @@ typedef struct ps_cand_batch {
                                        the bytes to move — what ps_eval_batch_host copies in    */
 } ps_cand_batch;
 
+/* Candidates as differences from one reference structure (host memory): the compact form of a
+   batch of neighbours — a candidate that differs from `ref` in d stage-order positions and f
+   offload bits costs 8d + 4f + 8 bytes instead of P*order_stride*2 + mask_words*4.
+   Candidate c = ref with orders[stage][pos] = code for every entry of
+   diffs[diff_offset[c] .. diff_offset[c+1]) (entry = stage << 16 | pos, code as a second word)
+   and every offload bit flips[flip_offset[c] .. flip_offset[c+1]) toggled (bit = i*m + j). */
+typedef struct ps_delta_batch {
+    int64_t num_candidates;
+    const uint16_t *ref_orders;     /* [P][order_stride]                                             */
+    const uint32_t *ref_mask;       /* [mask_words]                                                  */
+    const uint32_t *diff_offset;    /* [N+1], diff_offset[0] = 0                                     */
+    const uint32_t *diffs;          /* [diff_offset[N]][2]: (stage << 16 | pos, code)                */
+    const uint32_t *flip_offset;    /* [N+1]                                                         */
+    const uint32_t *flips;          /* [flip_offset[N]] offload bit indices                          */
+    const ps_base *base;            /* optional recorded base (as ps_cand_batch.base)                */
+} ps_delta_batch;
+
 /* Per-candidate outputs, device memory.  Optional arrays may be NULL. */
 typedef struct ps_result_batch {
     int64_t *makespan;              /* [N] makespan in time quanta, -1 unless FEASIBLE             */
@@ -144,6 +161,11 @@ typedef struct ps_search_desc {
     int32_t dedup;                  /* 1 (with a base, no makespan_out): a move drawn several times
                                        in the round is simulated once, by its lowest index — the
                                        round's best key is the same                              */
+    int64_t cutoff;                 /* > 0 (no makespan_out): the incumbent's makespan; a neighbour
+                                       whose makespan provably reaches it (every stage's free time
+                                       plus its remaining work) is abandoned — it
+                                       cannot be a strict improvement, so the selection is the
+                                       same.  0: every neighbour runs to its outcome.            */
 } ps_search_desc;
 
 /* A batch of branch-and-bound nodes (device buffers): the state solver._Search._bound reads. */
@@ -190,6 +212,12 @@ int ps_eval_batch(const ps_instance *inst, const ps_cand_batch *batch,
 int ps_eval_batch_host(const ps_instance *inst, const ps_cand_batch *batch,
                        const ps_result_batch *results, void *stream);
 
+/* ps_eval_batch_host on a delta-encoded batch (HOST buffers, results to HOST, synchronous): the
+   differences cross PCIe, the full candidates are rebuilt in HBM by a kernel and evaluated in
+   derived channel mode. */
+int ps_eval_batch_host_delta(const ps_instance *inst, const ps_delta_batch *batch,
+                             const ps_result_batch *results, void *stream);
+
 /* One local-search round over neighbours [first_index, first_index+count) of the incumbent:
    generate each move, evaluate it, and atomically fold (makespan << 32 | index) of every
    feasible neighbour into *best_key (device int64, caller initialises it to INT64_MAX).
@@ -207,6 +235,25 @@ int ps_search_round(const ps_instance *inst, const ps_search_desc *desc,
    reference's sequential selection loop (heuristics.py:206; solver.py:437) for one round. */
 int ps_search_round_sharded(const ps_instance *inst, const ps_search_desc *desc,
                             int64_t *best_key, int64_t *makespan_out, void *nccl_comm, void *stream);
+
+/* The channel-order search: the incumbent carries explicit per-channel transfer
+   orders inc_chan [G][chan_stride] (entries as in ps_cand_batch.channel_orders, padded with
+   0xFFFFFFFF), replayed in explicit channel mode (listsched.py:233-239).  A neighbour is a
+   stage-op shift (r0 % 1000 < shift_permille, or no transfers) or a shift of one transfer within
+   its channel order — a reload (or offload) moved earlier or later among the channel's
+   transfers (north star: "shift reloads").  Offload bits do not change.  Same key convention as
+   ps_search_round; neighbours are materialised and evaluated as explicit-channel batches (no
+   prefix sharing). */
+int ps_search_round_explicit(const ps_instance *inst, const ps_search_desc *desc, const uint32_t *inc_chan,
+                             int32_t chan_stride, int64_t *best_key, int64_t *makespan_out, void *stream);
+/* Neighbours [first_index, first_index+count) as full candidates: orders [count][P][stride],
+   masks [count][mask_words], channel orders [count][G][chan_stride] (device). */
+int ps_materialize_moves_explicit(const ps_instance *inst, const ps_search_desc *desc, const uint32_t *inc_chan,
+                                  int32_t chan_stride, uint16_t *orders_out, uint32_t *mask_out,
+                                  uint32_t *chan_out, void *stream);
+/* Apply neighbour `index` of `round` to the incumbent's stage and channel orders in place. */
+int ps_apply_move_explicit(const ps_instance *inst, uint16_t *inc_orders, uint32_t *inc_chan, int32_t chan_stride,
+                           const ps_move_params *moves, uint64_t round, uint64_t index, void *stream);
 
 /* Materialise neighbours [first_index, first_index+count) as full candidates (device buffers
    shaped like ps_cand_batch: orders [count][P][order_stride], masks [count][mask_words]). */

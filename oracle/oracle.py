@@ -66,6 +66,14 @@ def lib():
                                          C.POINTER(_Moves), C.c_uint64, C.c_int64, C.c_int64,
                                          C.c_void_p, C.c_int32]
         _lib.or_search_round.restype = C.c_int64
+        _lib.or_neighbour_explicit.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                               C.c_int32, C.POINTER(_Moves), C.c_uint64, C.c_uint64, C.c_void_p,
+                                               C.c_void_p, C.c_void_p]
+        _lib.or_neighbour_explicit.restype = C.c_int
+        _lib.or_search_round_explicit.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                                  C.c_int32, C.POINTER(_Moves), C.c_uint64, C.c_int64, C.c_int64,
+                                                  C.c_void_p, C.c_int32]
+        _lib.or_search_round_explicit.restype = C.c_int64
         _lib.or_bound.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32]
         _lib.or_bound.restype = C.c_int64
     return _lib
@@ -143,6 +151,32 @@ class Oracle:
                                         inc_m.ctypes.data, C.byref(mv), rnd, first, count,
                                         ms.ctypes.data if ms is not None else None, int(threads))
         return best, ms
+
+
+def neighbour_explicit(orc: "Oracle", inc_orders, inc_mask, inc_chan, seed, shift_permille, max_shift, rnd, index):
+    """Channel-order neighbour -> (type, orders, mask, chans)."""
+    inc_o = np.ascontiguousarray(inc_orders, np.uint16)
+    inc_m = np.ascontiguousarray(inc_mask, np.uint32)
+    inc_c = np.ascontiguousarray(inc_chan, np.uint32)
+    o, mk, ch = np.zeros_like(inc_o), np.zeros_like(inc_m), np.zeros_like(inc_c)
+    mv = _Moves(seed, shift_permille, max_shift)
+    t = orc.lib.or_neighbour_explicit(C.byref(orc._inst), inc_o.ctypes.data, inc_o.shape[-1], inc_m.ctypes.data,
+                                      inc_c.ctypes.data, inc_c.shape[-1], C.byref(mv), rnd, index, o.ctypes.data,
+                                      mk.ctypes.data, ch.ctypes.data)
+    return t, o, mk, ch
+
+
+def search_round_explicit(orc: "Oracle", inc_orders, inc_mask, inc_chan, seed, shift_permille, max_shift, rnd,
+                          first, count, threads=0, want_makespans=False):
+    inc_o = np.ascontiguousarray(inc_orders, np.uint16)
+    inc_m = np.ascontiguousarray(inc_mask, np.uint32)
+    inc_c = np.ascontiguousarray(inc_chan, np.uint32)
+    mv = _Moves(seed, shift_permille, max_shift)
+    ms = np.zeros(count, np.int64) if want_makespans else None
+    best = orc.lib.or_search_round_explicit(C.byref(orc._inst), inc_o.ctypes.data, inc_o.shape[-1], inc_m.ctypes.data,
+                                            inc_c.ctypes.data, inc_c.shape[-1], C.byref(mv), rnd, first, count,
+                                            ms.ctypes.data if ms is not None else None, int(threads))
+    return best, ms
 
 
 def bound(orc: "Oracle", t, sfree, start, post) -> int:

@@ -528,11 +528,66 @@ int or_neighbour(const or_instance *I, const uint16_t *inc, int32_t stride, cons
     return 2;
 }
 
+/* Channel-order neighbour: the search over explicit channel orders.  A stage-op
+ * SHIFT exactly as or_neighbour when r0 % 1000 < shift_permille (or no channel carries a
+ * transfer); otherwise RSHIFT: channel g = r1 % G, the transfer at position a = r2 % len_g moves
+ * to b = a -/+ d (d = 1 + (r3 >> 1) % max_shift, clamped), len_g = entries before the first
+ * 0xFFFFFFFF pad.  Offload bits never change.  Returns 0 no-op, 1 SHIFT, 3 RSHIFT. */
+int or_neighbour_explicit(const or_instance *I, const uint16_t *inc, int32_t stride, const uint32_t *inc_mask,
+                          const uint32_t *inc_chan, int32_t cstride, const or_moves *mv, uint64_t round,
+                          uint64_t index, uint16_t *out, uint32_t *mask_out, uint32_t *chan_out) {
+    const int P = I->P, m = I->m, G = I->G, Lo = 3 * m;
+    memcpy(out, inc, (size_t)P * stride * sizeof(uint16_t));
+    memcpy(mask_out, inc_mask, (size_t)((P * m + 31) / 32) * sizeof(uint32_t));
+    memcpy(chan_out, inc_chan, (size_t)G * cstride * sizeof(uint32_t));
+    int total = 0;
+    for (int g = 0; g < G; ++g)
+        for (int q = 0; q < cstride && inc_chan[(size_t)g * cstride + q] != 0xFFFFFFFFu; ++q) total++;
+    uint32_t ctr[4] = {(uint32_t)index, (uint32_t)(index >> 32), (uint32_t)round, (uint32_t)(round >> 32)};
+    uint32_t key[2] = {(uint32_t)mv->seed, (uint32_t)(mv->seed >> 32)};
+    uint32_t r[4];
+    or_philox4x32_10(ctr, key, r);
+    const uint32_t D = mv->max_shift ? mv->max_shift : 1u;
+    if (total == 0 || r[0] % 1000u < mv->shift_permille) {
+        int s = (int)(r[1] % (uint32_t)P);
+        int a = (int)(r[2] % (uint32_t)Lo);
+        int d = 1 + (int)((r[3] >> 1) % D);
+        int b = (r[3] & 1u) ? a - d : a + d;
+        if (b < 0) b = 0;
+        if (b > Lo - 1) b = Lo - 1;
+        if (b == a) return 0;
+        uint16_t *row = out + (size_t)s * stride;
+        uint16_t v = row[a];
+        if (a < b) memmove(row + a, row + a + 1, (size_t)(b - a) * sizeof(uint16_t));
+        else memmove(row + b + 1, row + b, (size_t)(a - b) * sizeof(uint16_t));
+        row[b] = v;
+        return 1;
+    }
+    int g = (int)(r[1] % (uint32_t)G);
+    int len = 0;
+    while (len < cstride && inc_chan[(size_t)g * cstride + len] != 0xFFFFFFFFu) len++;
+    if (len < 2) return 0;
+    int a = (int)(r[2] % (uint32_t)len);
+    int d = 1 + (int)((r[3] >> 1) % D);
+    int b = (r[3] & 1u) ? a - d : a + d;
+    if (b < 0) b = 0;
+    if (b > len - 1) b = len - 1;
+    if (b == a) return 0;
+    uint32_t *row = chan_out + (size_t)g * cstride;
+    uint32_t v = row[a];
+    if (a < b) memmove(row + a, row + a + 1, (size_t)(b - a) * sizeof(uint32_t));
+    else memmove(row + b + 1, row + b, (size_t)(a - b) * sizeof(uint32_t));
+    row[b] = v;
+    return 3;
+}
+
 typedef struct {
     const or_instance *I;
     const uint16_t *inc;
     int32_t stride;
     const uint32_t *inc_mask;
+    const uint32_t *inc_chan;   /* explicit channel-order search when non-NULL */
+    int32_t cstride;
     const or_moves *mv;
     uint64_t round;
     int64_t first;
@@ -544,6 +599,7 @@ typedef struct {
 typedef struct {
     uint16_t *ord;
     uint32_t *msk;
+    uint32_t *chn;
     int64_t best;
 } search_tls;
 
@@ -552,6 +608,7 @@ static void *search_tls_new(void *vctx) {
     search_tls *t = (search_tls *)malloc(sizeof(search_tls));
     t->ord = (uint16_t *)malloc((size_t)s->I->P * s->stride * sizeof(uint16_t));
     t->msk = (uint32_t *)malloc((size_t)((s->I->P * s->I->m + 31) / 32) * sizeof(uint32_t));
+    t->chn = s->inc_chan ? (uint32_t *)malloc((size_t)s->I->G * s->cstride * sizeof(uint32_t)) : NULL;
     t->best = INT64_MAX;
     return t;
 }
@@ -564,16 +621,21 @@ static void search_tls_done(void *vctx, void *vt) {
     pthread_mutex_unlock(&s->mu);
     free(t->ord);
     free(t->msk);
+    free(t->chn);
     free(t);
 }
 
 static void search_body(void *vctx, int64_t c, void *vt) {
     search_ctx *s = (search_ctx *)vctx;
     search_tls *t = (search_tls *)vt;
-    or_neighbour(s->I, s->inc, s->stride, s->inc_mask, s->mv, s->round, (uint64_t)(s->first + c), t->ord, t->msk);
+    if (s->inc_chan)
+        or_neighbour_explicit(s->I, s->inc, s->stride, s->inc_mask, s->inc_chan, s->cstride, s->mv, s->round,
+                              (uint64_t)(s->first + c), t->ord, t->msk, t->chn);
+    else
+        or_neighbour(s->I, s->inc, s->stride, s->inc_mask, s->mv, s->round, (uint64_t)(s->first + c), t->ord, t->msk);
     or_result r;
     memset(&r, 0, sizeof r);
-    or_run_order(s->I, t->ord, s->stride, t->msk, NULL, 0, &r);
+    or_run_order(s->I, t->ord, s->stride, t->msk, t->chn, s->inc_chan ? s->cstride : 0, &r);
     if (s->makespans) s->makespans[c] = r.flags == 1 ? r.makespan : -1;
     if (r.flags == 1) {
         int64_t key = (r.makespan << 32) | (int64_t)(uint32_t)(s->first + c);
@@ -584,8 +646,15 @@ static void search_body(void *vctx, int64_t c, void *vt) {
 int64_t or_search_round(const or_instance *I, const uint16_t *inc, int32_t stride, const uint32_t *inc_mask,
                         const or_moves *mv, uint64_t round, int64_t first, int64_t count, int64_t *makespans,
                         int32_t threads) {
+    return or_search_round_explicit(I, inc, stride, inc_mask, NULL, 0, mv, round, first, count, makespans, threads);
+}
+
+int64_t or_search_round_explicit(const or_instance *I, const uint16_t *inc, int32_t stride, const uint32_t *inc_mask,
+                                 const uint32_t *inc_chan, int32_t cstride, const or_moves *mv, uint64_t round,
+                                 int64_t first, int64_t count, int64_t *makespans, int32_t threads) {
     search_ctx s;
     s.I = I; s.inc = inc; s.stride = stride; s.inc_mask = inc_mask; s.mv = mv; s.round = round;
+    s.inc_chan = inc_chan; s.cstride = cstride;
     s.first = first; s.makespans = makespans; s.best = INT64_MAX;
     pthread_mutex_init(&s.mu, NULL);
     pool_run(threads, count, search_body, search_tls_new, search_tls_done, &s);

@@ -80,6 +80,19 @@ class CandBatch(C.Structure):
     ]
 
 
+class DeltaBatch(C.Structure):
+    _fields_ = [
+        ("num_candidates", C.c_int64),
+        ("ref_orders", C.c_void_p),
+        ("ref_mask", C.c_void_p),
+        ("diff_offset", C.c_void_p),
+        ("diffs", C.c_void_p),
+        ("flip_offset", C.c_void_p),
+        ("flips", C.c_void_p),
+        ("base", C.c_void_p),
+    ]
+
+
 class ResultBatch(C.Structure):
     _fields_ = [
         ("makespan", C.c_void_p),
@@ -113,6 +126,7 @@ class SearchDesc(C.Structure):
         ("events_total", C.c_void_p),
         ("base", C.c_void_p),
         ("dedup", C.c_int32),
+        ("cutoff", C.c_int64),
     ]
 
 
@@ -136,6 +150,13 @@ EXPORTS = {
     "ps_search_round": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
     "ps_search_round_sharded": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]),
+    "ps_eval_batch_host_delta": (C.c_int, [C.c_void_p, C.POINTER(DeltaBatch), C.POINTER(ResultBatch), C.c_void_p]),
+    "ps_search_round_explicit": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_int32,
+                                           C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_materialize_moves_explicit": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_int32,
+                                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_apply_move_explicit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(MoveParams),
+                                         C.c_uint64, C.c_uint64, C.c_void_p]),
     "ps_materialize_moves": (C.c_int, [C.c_void_p, C.POINTER(SearchDesc), C.c_void_p, C.c_void_p, C.c_void_p]),
     "ps_apply_move": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(MoveParams),
                                 C.c_uint64, C.c_uint64, C.c_void_p]),

@@ -5,6 +5,7 @@
 #include <nvtx3/nvToolsExt.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <climits>
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -134,7 +135,6 @@ struct Plan {
     int K, warps;
     bool gstate;
     int cand_words, inc_words;
-    int dirty_words = 0;
     LaunchCfg cfg;
     size_t scratch_bytes;
 };
@@ -237,9 +237,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
         pl->gstate = true;
         pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
-        // (move mode) each warp's dirty bitmap of its slot's end-time words (ps_eval.cuh TRACK)
-        pl->dirty_words = moves && env_int("PS_GSTATE_TRACK", 1) ? (((2 * I->P * I->m + 31) / 32 + 3) & ~3) : 0;
-        pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * pl->dirty_words) * 4;
+        pl->cfg.smem = (size_t)pl->inc_words * 4;
         pl->cfg.block = 32 * pl->warps;
     };
     int per_sm = 0, rc;
@@ -342,7 +340,6 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.K = pl.K;
         q.cand_words = pl.cand_words;
         q.inc_words = pl.inc_words;
-        q.dirty_words = pl.gstate ? pl.dirty_words : 0;
         int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order;         // handoff k-1
         int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
         q.work_count = in;
@@ -995,6 +992,115 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
     return PS_OK;
 }
 
+// ---- delta-encoded host batches: rebuild full candidates in HBM -------------------------------
+
+// One warp per (candidate, stage): copy the reference row; the stage-0 warp copies the mask.
+__global__ void delta_rows_kernel(int64_t N, int P, int stride, int mask_words, const uint16_t *ref,
+                                  const uint32_t *ref_mask, uint16_t *out, uint32_t *out_mask) {
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= N * P) return;
+    const int64_t c = row / P;
+    const int s = (int)(row % P);
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(ref + (size_t)s * stride);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(out + ((size_t)c * P + s) * stride);
+    for (int q = lane; q < stride / 2; q += 32) dst[q] = src[q];
+    if (s == 0)
+        for (int w = lane; w < mask_words; w += 32) out_mask[(size_t)c * mask_words + w] = ref_mask[w];
+}
+
+// One thread per candidate: apply its differences (after delta_rows_kernel, same stream).
+__global__ void delta_apply_kernel(int64_t N, int P, int stride, int mask_words, const uint32_t *doff,
+                                   const uint32_t *diffs, const uint32_t *foff, const uint32_t *flips,
+                                   uint16_t *out, uint32_t *out_mask) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    for (uint32_t k = doff[c]; k < doff[c + 1]; ++k) {
+        const uint32_t e = diffs[2 * (size_t)k];
+        out[((size_t)c * P + (e >> 16)) * stride + (e & 0xFFFFu)] = (uint16_t)diffs[2 * (size_t)k + 1];
+    }
+    for (uint32_t k = foff[c]; k < foff[c + 1]; ++k) {
+        const uint32_t b = flips[k];
+        out_mask[(size_t)c * mask_words + (b >> 5)] ^= 1u << (b & 31);
+    }
+}
+
+int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, const ps_result_batch *r, void *stream) {
+    NvtxRange nvtx("ps_eval_batch_host_delta n=%llu", (unsigned long long)(b ? b->num_candidates : 0));
+    if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
+    const int64_t N = b->num_candidates;
+    if (N <= 0) return N == 0 ? PS_OK : fail(PS_ERR_INVALID, "negative candidate count");
+    if (!b->ref_orders || !b->ref_mask || !b->diff_offset || !b->flip_offset)
+        return fail(PS_ERR_INVALID, "ref_orders, ref_mask, diff_offset and flip_offset are required");
+    if (r->events_total) return fail(PS_ERR_INVALID, "events_total is a device counter: use ps_eval_batch");
+    const uint64_t nd = b->diff_offset[N], nf = b->flip_offset[N];
+    if ((nd && !b->diffs) || (nf && !b->flips)) return fail(PS_ERR_INVALID, "diffs / flips missing");
+    for (int64_t c = 0; c < N; ++c)
+        if (b->diff_offset[c + 1] < b->diff_offset[c] || b->flip_offset[c + 1] < b->flip_offset[c])
+            return fail(PS_ERR_INVALID, "offsets must be non-decreasing");
+    for (uint64_t k = 0; k < nd; ++k) {
+        const uint32_t e = b->diffs[2 * k];
+        if ((int)(e >> 16) >= I->P || (int)(e & 0xFFFFu) >= I->L) return fail(PS_ERR_INVALID, "diff %llu out of range", (unsigned long long)k);
+    }
+    for (uint64_t k = 0; k < nf; ++k)
+        if (b->flips[k] >= (uint32_t)(I->P * I->m)) return fail(PS_ERR_INVALID, "flip %llu out of range", (unsigned long long)k);
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    // device arena: the encoded batch, then the rebuilt candidates and the outputs
+    const size_t n_ref = (size_t)I->P * I->stride * 2, n_rmask = (size_t)I->mask_words * 4;
+    const size_t n_off = (size_t)(N + 1) * 4, n_diff = (size_t)nd * 8, n_flip = (size_t)nf * 4;
+    const size_t n_ord = (size_t)N * I->P * I->stride * 2, n_mask = (size_t)N * I->mask_words * 4;
+    const size_t n_peak = r->peak ? (size_t)N * I->P * 8 : 0, n_blk = r->blocked ? (size_t)N * 4 : 0;
+    size_t sizes[13] = {n_ref, n_rmask, n_off, n_diff, n_off, n_flip, n_ord, n_mask, (size_t)N * 8, (size_t)N * 8,
+                        n_peak, (size_t)N * 4, n_blk};
+    size_t off[13], total = 0;
+    for (int k = 0; k < 13; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
+    char *arena = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
+    const void *srcs[6] = {b->ref_orders, b->ref_mask, b->diff_offset, b->diffs, b->flip_offset, b->flips};
+    for (int k = 0; k < 6; ++k)
+        if (sizes[k]) PS_CUDA(cudaMemcpyAsync(arena + off[k], srcs[k], sizes[k], cudaMemcpyHostToDevice, s));
+    uint16_t *ord = (uint16_t *)(arena + off[6]);
+    uint32_t *msk = (uint32_t *)(arena + off[7]);
+    const int64_t warps = N * I->P;
+    delta_rows_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+        N, I->P, I->stride, I->mask_words, (const uint16_t *)(arena + off[0]), (const uint32_t *)(arena + off[1]), ord, msk);
+    delta_apply_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(
+        N, I->P, I->stride, I->mask_words, (const uint32_t *)(arena + off[2]), (const uint32_t *)(arena + off[3]),
+        (const uint32_t *)(arena + off[4]), (const uint32_t *)(arena + off[5]), ord, msk);
+    PS_CUDA(cudaGetLastError());
+    ps_cand_batch db;
+    memset(&db, 0, sizeof db);
+    db.num_candidates = N;
+    db.stage_orders = ord;
+    db.offload_mask = msk;
+    db.base = b->base;
+    db.order_bytes = 2;
+    ps_result_batch dr = *r;
+    dr.makespan = (int64_t *)(arena + off[8]);
+    dr.bubble = (double *)(arena + off[9]);
+    dr.peak = n_peak ? (int64_t *)(arena + off[10]) : nullptr;
+    dr.flags = (uint32_t *)(arena + off[11]);
+    dr.blocked = n_blk ? (uint32_t *)(arena + off[12]) : nullptr;
+    dr.trace_code = nullptr;
+    dr.trace_start = nullptr;
+    dr.trace_stride = 0;
+    int rc = eval_batch_impl(I, &db, &dr, s, nullptr, 0);
+    if (rc == PS_OK) {
+        PS_CUDA(cudaMemcpyAsync(r->makespan, dr.makespan, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(r->bubble, dr.bubble, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(r->flags, dr.flags, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
+        if (n_peak) PS_CUDA(cudaMemcpyAsync(r->peak, dr.peak, n_peak, cudaMemcpyDeviceToHost, s));
+        if (n_blk) PS_CUDA(cudaMemcpyAsync(r->blocked, dr.blocked, n_blk, cudaMemcpyDeviceToHost, s));
+    }
+    cudaFreeAsync(arena, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "ps_eval_batch_host_delta");
+    return PS_OK;
+}
+
 // Pinned host word holding 1: the copy engine writes it behind each chunk as its ready flag.
 static const int32_t *pinned_one() {
     static int32_t *one = nullptr;
@@ -1146,8 +1252,125 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.makespan = makespan_out;
     p.best_key = (long long *)best_key;
     p.dedup = makespan_out == nullptr && d->dedup;
+    p.cutoff = makespan_out == nullptr && d->cutoff > 0 ? d->cutoff : 0;
     p.events_total = (unsigned long long *)d->events_total;
     return run_eval(I, p, true, (cudaStream_t)stream, d->base);
+}
+
+// ---- channel-order search: explicit channel orders, reload/offload shifts ----
+
+struct XMove {
+    int type;          // 0 no-op, 1 stage-op SHIFT, 3 transfer RSHIFT
+    int row, a, b;     // stage (SHIFT) or channel (RSHIFT); element at a moves to b
+};
+
+// lens[g] = transfers in the incumbent's channel g (entries before the first pad), lens[G] = total.
+__global__ void chan_lens_kernel(const uint32_t *inc_chan, int G, int cstride, int *lens) {
+    __shared__ int tot;
+    if (threadIdx.x == 0) tot = 0;
+    __syncthreads();
+    for (int g = threadIdx.x; g < G; g += blockDim.x) {
+        int n = 0;
+        while (n < cstride && inc_chan[(size_t)g * cstride + n] != 0xFFFFFFFFu) ++n;
+        lens[g] = n;
+        atomicAdd(&tot, n);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) lens[G] = tot;
+}
+
+// The move of neighbour `index` (oracle/ps_oracle.c or_neighbour_explicit restates it).
+__device__ XMove decode_xmove(const ps_move_params &mp, uint64_t round, uint64_t index, int P, int L, int G,
+                              const int *lens) {
+    Philox4 r = philox4x32_10((uint32_t)index, (uint32_t)(index >> 32), (uint32_t)round, (uint32_t)(round >> 32),
+                              (uint32_t)mp.seed, (uint32_t)(mp.seed >> 32));
+    const uint32_t D = mp.max_shift ? mp.max_shift : 1u;
+    XMove mv;
+    mv.type = 0;
+    mv.a = mv.b = 0;
+    int n;
+    const bool stage_move = lens[G] == 0 || r.v[0] % 1000u < mp.shift_permille;
+    if (stage_move) {
+        mv.row = (int)(r.v[1] % (uint32_t)P);
+        n = L;
+    } else {
+        mv.row = (int)(r.v[1] % (uint32_t)G);
+        n = lens[mv.row];
+        if (n < 2) return mv;
+    }
+    const int a = (int)(r.v[2] % (uint32_t)n);
+    const int d = 1 + (int)((r.v[3] >> 1) % D);
+    int b = (r.v[3] & 1u) ? a - d : a + d;
+    b = b < 0 ? 0 : (b > n - 1 ? n - 1 : b);
+    mv.a = a;
+    mv.b = b;
+    if (b != a) mv.type = stage_move ? 1 : 3;
+    return mv;
+}
+
+// One warp per (neighbour, row): rows [0, P) are stage orders, [P, P + G) channel orders; the
+// stage-0 warp also writes the (unchanged) offload mask.
+__global__ void materialize_x_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first, int64_t count,
+                                     int G, int cstride, const int *lens, const uint16_t *inc,
+                                     const uint32_t *inc_mask, const uint32_t *inc_chan, uint16_t *out,
+                                     uint32_t *out_mask, uint32_t *out_chan) {
+    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int R = c.P + G;
+    if (row >= count * R) return;
+    const int64_t n = row / R;
+    const int r = (int)(row % R);
+    const XMove mv = decode_xmove(mp, round, (uint64_t)(first + n), c.P, c.L, G, lens);
+    if (r < c.P) {
+        const bool sh = mv.type == 1 && mv.row == r;
+        const uint16_t *src = inc + (size_t)r * c.stride;
+        uint16_t *dst = out + ((size_t)n * c.P + r) * c.stride;
+        for (int q = lane; q < c.stride; q += 32)
+            dst[q] = q < c.L ? src[sh ? shifted_position(q, mv.a, mv.b) : q] : (uint16_t)0;
+        if (r == 0)
+            for (int w = lane; w < c.mask_words; w += 32) out_mask[(size_t)n * c.mask_words + w] = inc_mask[w];
+    } else {
+        const int g = r - c.P;
+        const bool sh = mv.type == 3 && mv.row == g;
+        const uint32_t *src = inc_chan + (size_t)g * cstride;
+        uint32_t *dst = out_chan + ((size_t)n * G + g) * cstride;
+        for (int q = lane; q < cstride; q += 32) dst[q] = src[sh && q < lens[g] ? shifted_position(q, mv.a, mv.b) : q];
+    }
+}
+
+__global__ void apply_x_kernel(MoveCtx c, ps_move_params mp, uint64_t round, uint64_t index, int G, int cstride,
+                               const int *lens, uint16_t *inc, uint32_t *inc_chan) {
+    if (threadIdx.x) return;
+    const XMove mv = decode_xmove(mp, round, index, c.P, c.L, G, lens);
+    if (mv.type == 1) {
+        uint16_t *row = inc + (size_t)mv.row * c.stride;
+        const uint16_t v = row[mv.a];
+        if (mv.a < mv.b) for (int q = mv.a; q < mv.b; ++q) row[q] = row[q + 1];
+        else for (int q = mv.a; q > mv.b; --q) row[q] = row[q - 1];
+        row[mv.b] = v;
+    } else if (mv.type == 3) {
+        uint32_t *row = inc_chan + (size_t)mv.row * cstride;
+        const uint32_t v = row[mv.a];
+        if (mv.a < mv.b) for (int q = mv.a; q < mv.b; ++q) row[q] = row[q + 1];
+        else for (int q = mv.a; q > mv.b; --q) row[q] = row[q - 1];
+        row[mv.b] = v;
+    }
+}
+
+// best_key = min over feasible neighbours of (makespan << 32 | global index)
+__global__ void best_key_kernel(const int64_t *makespan, const uint32_t *flags, int64_t n, int64_t first,
+                                long long *best_key) {
+    long long best = LLONG_MAX;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        if (flags[k] == FLAG_FEASIBLE) {
+            const long long key = ((long long)makespan[k] << 32) | (long long)(uint32_t)(first + k);
+            best = key < best ? key : best;
+        }
+    for (int o = 16; o; o >>= 1) {
+        const long long v = __shfl_xor_sync(0xffffffffu, best, o);
+        best = v < best ? v : best;
+    }
+    if ((threadIdx.x & 31) == 0 && best != LLONG_MAX) atomicMin(best_key, best);
 }
 
 // NCCL, resolved at run time: the library stays loadable on hosts without NCCL, and shares the
@@ -1184,6 +1407,117 @@ int ps_search_round_sharded(const ps_instance *I, const ps_search_desc *d, int64
     if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
     ncclResult_t r = ar(best_key, best_key, 1, ncclInt64, ncclMin, (ncclComm_t)nccl_comm, (cudaStream_t)stream);
     if (r != ncclSuccess) return fail(PS_ERR_CUDA, "ncclAllReduce: %s", es ? es(r) : "error");
+    return PS_OK;
+}
+
+static int check_x(const ps_instance *I, const uint32_t *inc_chan, int chan_stride) {
+    if (!inc_chan) return fail(PS_ERR_INVALID, "the incumbent's channel orders are required");
+    if (chan_stride < 1) return fail(PS_ERR_INVALID, "chan_stride must be positive");
+    return PS_OK;
+}
+
+int ps_materialize_moves_explicit(const ps_instance *I, const ps_search_desc *d, const uint32_t *inc_chan,
+                                  int32_t chan_stride, uint16_t *orders_out, uint32_t *mask_out, uint32_t *chan_out,
+                                  void *stream) {
+    NvtxRange nvtx("ps_materialize_moves_explicit");
+    if (!I || !d || !orders_out || !mask_out || !chan_out) return fail(PS_ERR_INVALID, "null argument");
+    int rc = check_x(I, inc_chan, chan_stride);
+    if (rc) return rc;
+    if (d->count <= 0) return PS_OK;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int *lens = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&lens, (I->G + 1) * sizeof(int), s));
+    chan_lens_kernel<<<1, 32, 0, s>>>(inc_chan, I->G, chan_stride, lens);
+    const int64_t warps = d->count * (I->P + I->G);
+    materialize_x_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+        move_ctx(I), d->moves, d->round, d->first_index, d->count, I->G, chan_stride, lens, d->inc_orders, d->inc_mask,
+        inc_chan, orders_out, mask_out, chan_out);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA(cudaFreeAsync(lens, s));
+    return PS_OK;
+}
+
+int ps_apply_move_explicit(const ps_instance *I, uint16_t *inc_orders, uint32_t *inc_chan, int32_t chan_stride,
+                           const ps_move_params *mp, uint64_t round, uint64_t index, void *stream) {
+    NvtxRange nvtx("ps_apply_move_explicit");
+    if (!I || !inc_orders || !mp) return fail(PS_ERR_INVALID, "null argument");
+    int rc = check_x(I, inc_chan, chan_stride);
+    if (rc) return rc;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int *lens = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&lens, (I->G + 1) * sizeof(int), s));
+    chan_lens_kernel<<<1, 32, 0, s>>>(inc_chan, I->G, chan_stride, lens);
+    apply_x_kernel<<<1, 32, 0, s>>>(move_ctx(I), *mp, round, index, I->G, chan_stride, lens, inc_orders, inc_chan);
+    PS_CUDA(cudaGetLastError());
+    PS_CUDA(cudaFreeAsync(lens, s));
+    return PS_OK;
+}
+
+int ps_search_round_explicit(const ps_instance *I, const ps_search_desc *d, const uint32_t *inc_chan,
+                             int32_t chan_stride, int64_t *best_key, int64_t *makespan_out, void *stream) {
+    NvtxRange nvtx("ps_search_round_explicit r=%llu", (unsigned long long)(d ? d->round : 0));
+    if (!I || !d || !best_key) return fail(PS_ERR_INVALID, "null argument");
+    if (!d->inc_orders || !d->inc_mask) return fail(PS_ERR_INVALID, "incumbent buffers are required");
+    int rc = check_x(I, inc_chan, chan_stride);
+    if (rc) return rc;
+    if (d->count < 0 || d->first_index < 0) return fail(PS_ERR_INVALID, "negative shard range");
+    if ((uint64_t)(d->first_index + d->count) > 0xFFFFFFFFull)
+        return fail(PS_ERR_RANGE, "neighbour indices must stay below 2^32");
+    if (d->moves.shift_permille > 1000u || d->moves.max_shift < 1u)
+        return fail(PS_ERR_INVALID, "shift_permille must be <= 1000 and max_shift >= 1");
+    if (d->count == 0) return PS_OK;
+    DeviceGuard guard(I->device);
+    if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    // neighbours are materialised in chunks (stage rows + channel rows) and evaluated as an
+    // explicit-channel batch; each chunk's best key folds into *best_key
+    const int64_t chunk = std::min<int64_t>(d->count, std::max(256, env_int("PS_X_CHUNK", 16384)));
+    const size_t ord_b = (size_t)chunk * I->P * I->stride * 2, msk_b = (size_t)chunk * I->mask_words * 4;
+    const size_t chn_b = (size_t)chunk * I->G * chan_stride * 4;
+    char *arena = nullptr;
+    const size_t total = ord_b + msk_b + chn_b + (size_t)chunk * (8 + 8 + 4) + (I->G + 1) * 4 + 1024;
+    PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
+    size_t off = 0;
+    auto take = [&](size_t n) { char *q = arena + off; off += (n + 255) & ~(size_t)255; return q; };
+    uint16_t *ord = (uint16_t *)take(ord_b);
+    uint32_t *msk = (uint32_t *)take(msk_b);
+    uint32_t *chn = (uint32_t *)take(chn_b);
+    int64_t *span = (int64_t *)take((size_t)chunk * 8);
+    double *bub = (double *)take((size_t)chunk * 8);
+    uint32_t *flg = (uint32_t *)take((size_t)chunk * 4);
+    int *lens = (int *)take((I->G + 1) * 4);
+    (void)total;
+    chan_lens_kernel<<<1, 32, 0, s>>>(inc_chan, I->G, chan_stride, lens);
+    for (int64_t lo = 0; lo < d->count; lo += chunk) {
+        const int64_t n = std::min(chunk, d->count - lo);
+        const int64_t warps = n * (I->P + I->G);
+        materialize_x_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+            move_ctx(I), d->moves, d->round, d->first_index + lo, n, I->G, chan_stride, lens, d->inc_orders,
+            d->inc_mask, inc_chan, ord, msk, chn);
+        PS_CUDA(cudaGetLastError());
+        EvalParams p;
+        memset(&p, 0, sizeof p);
+        fill_instance(I, &p);
+        p.N = n;
+        p.orders = ord;
+        p.masks = msk;
+        p.chorders = chn;
+        p.chan_stride = chan_stride;
+        p.makespan = makespan_out ? makespan_out + lo : span;
+        p.bubble = bub;
+        p.flags = flg;
+        p.events_total = (unsigned long long *)d->events_total;
+        rc = run_eval(I, p, false, s, nullptr);
+        if (rc) return rc;
+        best_key_kernel<<<std::max(1, std::min((int)((n + 255) / 256), 4 * I->num_sms)), 256, 0, s>>>(
+            p.makespan, flg, n, d->first_index + lo, (long long *)best_key);
+        PS_CUDA(cudaGetLastError());
+    }
+    PS_CUDA(cudaFreeAsync(arena, s));
     return PS_OK;
 }
 

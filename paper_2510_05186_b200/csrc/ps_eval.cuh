@@ -82,6 +82,7 @@ struct EvalParams {
     const int32_t *ready;
     long long ready_chunk;
     int dedup;               // (host side) evaluate each distinct move of a round once
+    long long cutoff;        // > 0: abandon a neighbour whose makespan bound reaches it (§3.13)
     const int32_t *work_list;
     const int32_t *work_count;
     // per-candidate state
@@ -306,6 +307,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     V rF = NO_R, rG = NO_R;
     int tauF = 0, tauG = 0;
     int first_start = INT_MAX;      // start of the stage's first op (always an F; its last op is always a W)
+    int rem = 0;                    // (bound pruning) work of this stage's uncommitted ops
     int ecount = 0, ecount0 = 0;             // events committed / restored from a checkpoint
     int cc = 0;                              // compute events committed (checkpoints count these)
     uint32_t head = 0, nxt = 0;
@@ -1041,6 +1043,17 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             first_start = INT_MAX; ecount = 0;
             cc = 0;
         }
+        // Bound pruning (search rounds with a cutoff): the stage's remaining work
+        const bool prune = MOVES && !REC && p.cutoff > 0;
+        if (prune) {
+            rem = 0;
+            if (has_stage)
+                for (int q = pos; q < L; ++q) {
+                    const uint32_t op = fetch(q);
+                    rem += proc_of((int)(op >> 2), (int)(op & 3u));
+                }
+        }
+        bool pruned = false;
         const int cc0 = cc;
         ovf = false;
         rF = rG = NO_R;
@@ -1069,6 +1082,21 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 const int nx = __shfl_sync(0xffffffffu, wt, min(i + 1, 31));
                 const bool stuck = wt == i || (wt == i + 1 && nx == i);      // (wt >= 0: no key)
                 if (__any_sync(0xffffffffu, stuck)) { early_dl = true; break; }
+                if (prune) {
+                    // every remaining op of a stage runs after its free time: the makespan is at
+                    // least max(free + remaining work) - min(first start) (per-stage spans under
+                    // post-validation); no strict improvement once that reaches the incumbent's
+                    long long lb;
+                    if (p.post) {
+                        lb = __reduce_max_sync(0xffffffffu, has_stage && first_start != INT_MAX
+                                                                ? (unsigned)(sfree + rem - first_start) : 0u);
+                    } else {
+                        const int hi = (int)__reduce_max_sync(0xffffffffu, has_stage ? (unsigned)(sfree + rem) : 0u);
+                        const int lo = (int)__reduce_min_sync(0xffffffffu, has_stage ? (unsigned)first_start : 0x7FFFFFFFu);
+                        lb = (long long)hi - (long long)lo;
+                    }
+                    if (lb >= p.cutoff) { pruned = true; break; }
+                }
             }
             if (tdirty) { transfer_key(); tdirty = false; }
             const unsigned long long key = min(ckey, tkey);
@@ -1139,6 +1167,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             if (rank == RANK_COMPUTE) {
                 if (i == w) {
                     const int end = t + proc_of(j, k);
+                    rem -= end - t;
                     const bool newreq = derived && k == KIND_F && ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u);
                     win_insert(end, val_of(j, k));
                     sfree = end;
@@ -1286,6 +1315,13 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                     if (key < *(volatile long long *)p.best_key) atomicMin(p.best_key, key);
                 }
             }
+            __syncwarp();
+            continue;
+        }
+        if (pruned) {
+            // cannot improve on the incumbent: no key, no outputs (search rounds request none)
+            if (lane == 0 && p.events_total && ecount > ecount0)
+                atomicAdd(p.events_total, (unsigned long long)(ecount - ecount0));
             __syncwarp();
             continue;
         }

@@ -135,6 +135,27 @@ class DeviceInstance:
         del h_orders, h_masks, h_chans
         return out
 
+    def evaluate_host_delta(self, ref_orders, ref_mask, diff_offset, diffs, flip_offset, flips, peak=True,
+                            out: EvalResult | None = None, stream=None, base: "Base | None" = None) -> EvalResult:
+        """A host batch given as differences from one reference structure (packing.delta_encode):
+        only the differences cross PCIe (ps_eval_batch_host_delta)."""
+        n = int(len(diff_offset)) - 1
+        if out is None:
+            out = EvalResult(np.empty(n, np.int64), np.empty(n, np.float64), np.empty(n, np.int32),
+                             np.empty((n, self.P), np.int64) if peak else None, np.empty(n, np.int32))
+        keep = [np.ascontiguousarray(ref_orders, np.uint16), np.ascontiguousarray(ref_mask, np.uint32),
+                np.ascontiguousarray(diff_offset, np.uint32), np.ascontiguousarray(diffs, np.uint32),
+                np.ascontiguousarray(flip_offset, np.uint32), np.ascontiguousarray(flips, np.uint32)]
+        pk = self.packed
+        if keep[0].shape != (pk.num_stages, pk.order_stride) or keep[1].shape != (pk.mask_words,):
+            raise ValueError("reference structure has the wrong shape")
+        db = N.DeltaBatch(n, *[a.ctypes.data for a in keep], base.handle if base is not None else None)
+        rb = N.ResultBatch(_ptr(out.makespan), _ptr(out.bubble), _ptr(out.peak), _ptr(out.flags),
+                           _ptr(out.blocked), None, None, 0, None)
+        N.check(self.lib.ps_eval_batch_host_delta(self.handle, C.byref(db), C.byref(rb), self._stream(stream)))
+        del keep
+        return out
+
     def _check_batch(self, n, orders, masks, chans, host):
         """Shapes and element types the C ABI reads (include/pipesched_b200.h ps_cand_batch):
         orders [N][P][order_stride] of uint16 (or uint8 when 4m <= 256), masks [N][mask_words]

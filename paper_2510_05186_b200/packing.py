@@ -183,3 +183,34 @@ def decode_mask(pk: PackedInstance, mask_row: np.ndarray) -> frozenset:
         if (int(mask_row[b >> 5]) >> (b & 31)) & 1:
             out.append(OpId(b // m + 1, b % m + 1, OpKind.F))
     return frozenset(out)
+
+
+def delta_encode(ref_orders: np.ndarray, ref_mask: np.ndarray, orders: np.ndarray, masks: np.ndarray,
+                 chunk: int = 4096):
+    """A batch as differences from one reference structure (ps_delta_batch): returns
+    (diff_offset uint32 [N+1], diffs uint32 [D][2] = (stage << 16 | pos, code),
+     flip_offset uint32 [N+1], flips uint32 [F] = offload bit index)."""
+    n = int(orders.shape[0])
+    ref_orders = np.asarray(ref_orders, np.uint16)
+    ref_mask = np.asarray(ref_mask, np.uint32)
+    d_parts, f_parts = [], []
+    dcount = np.zeros(n, np.int64)
+    fcount = np.zeros(n, np.int64)
+    for lo in range(0, n, chunk):
+        o = np.asarray(orders[lo:lo + chunk]).view(np.uint16)
+        nn, ss, pp = np.nonzero(o != ref_orders[None])
+        dcount[lo:lo + len(o)] = np.bincount(nn, minlength=len(o))
+        d_parts.append(np.stack([(ss.astype(np.uint32) << 16) | pp.astype(np.uint32),
+                                 o[nn, ss, pp].astype(np.uint32)], axis=1))
+        x = np.asarray(masks[lo:lo + chunk]).view(np.uint32) ^ ref_mask[None]
+        bits = np.unpackbits(x.view(np.uint8), axis=1, bitorder="little")
+        cn, cb = np.nonzero(bits)
+        fcount[lo:lo + len(o)] = np.bincount(cn, minlength=len(o))
+        f_parts.append(cb.astype(np.uint32))
+    doff = np.zeros(n + 1, np.uint32)
+    doff[1:] = np.cumsum(dcount)
+    foff = np.zeros(n + 1, np.uint32)
+    foff[1:] = np.cumsum(fcount)
+    diffs = np.ascontiguousarray(np.concatenate(d_parts) if d_parts else np.zeros((0, 2), np.uint32))
+    flips = np.ascontiguousarray(np.concatenate(f_parts) if f_parts else np.zeros(0, np.uint32))
+    return doff, diffs, foff, flips

@@ -37,6 +37,7 @@ class SearchConfig:
     max_shift: int = 4
     share_prefix: bool = True        # resume neighbours from checkpoints of the incumbent
     dedup: bool = True               # simulate a move drawn several times in a round once
+    prune: bool = True               # abandon neighbours that provably cannot improve
     # Iterated local search: after `descent_patience` rounds without improving
     # the current point, restart the descent from the best structure kicked by `kick_moves`
     # random moves.  0 = plain descent (a run then ends at convergence or its budget).
@@ -189,7 +190,8 @@ class LocalSearch:
         self.best_key.fill_(N.BEST_NONE)
         desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round,
                             self.first, self.count, self.moves, None,
-                            self.base.handle if self.base is not None else None, int(self.cfg.dedup))
+                            self.base.handle if self.base is not None else None, int(self.cfg.dedup),
+                            self.makespan if self.cfg.prune and makespan_out is None else 0)
         ms = C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None
         if self.nccl_comm:
             N.check(self.lib.ps_search_round_sharded(self.di.handle, C.byref(desc), C.c_void_p(self.best_key.data_ptr()),
@@ -369,3 +371,136 @@ def warm_start_search(inst, config: SearchConfig = SearchConfig(), rounds=None, 
     orders = {i: stage_order_of(s, i) for i in range(1, inst.num_stages + 1)}
     ls = LocalSearch(inst, orders, s.offloaded, config, device=device, group=group)
     return ls.run(rounds=rounds, time_budget=time_budget, patience=patience)
+
+
+class ChannelSearch:
+    """The channel-order search: the incumbent carries explicit per-channel
+    transfer orders, replayed in explicit channel mode (listsched.py:233-239), and a neighbour
+    shifts either one op of a stage order or one transfer — a reload or an offload — within its
+    channel's order (``ps_search_round_explicit``).  Offload bits stay fixed.  Start it from a
+    timed schedule (``from_schedule``): its channel orders replay it exactly.  Same selection
+    rules as LocalSearch (lowest index on ties, strict improvement), no prefix sharing."""
+
+    def __init__(self, inst, stage_orders, offloaded, channel_orders, config: SearchConfig = SearchConfig(),
+                 device=None):
+        import torch
+        from .packing import encode_candidate
+        self.inst = inst
+        self.cfg = config
+        self.di = device_instance(inst, device)
+        self.lib = self.di.lib
+        pk = self.di.packed
+        o, mk, ch = encode_candidate(pk, stage_orders, offloaded, channel_orders)
+        # room for every channel's transfers (2 per offloaded F of its stages)
+        width = max([ch.shape[1]] + [1])
+        dev = torch.device("cuda", self.di.device)
+        self.chan_stride = int(width)
+        self.inc_orders = torch.from_numpy(o.view(np.int16).copy()).to(dev)
+        self.inc_mask = torch.from_numpy(mk.view(np.int32).copy()).to(dev)
+        self.inc_chan = torch.from_numpy(np.ascontiguousarray(ch).view(np.int32).copy()).to(dev)
+        self.best_key = torch.empty(1, dtype=torch.int64, device=dev)
+        self.moves = N.MoveParams(config.seed & (2**64 - 1), config.shift_permille, config.max_shift)
+        res = self.di.evaluate(self.inc_orders.view(1, *self.inc_orders.shape), self.inc_mask.view(1, -1),
+                               self.inc_chan.view(1, *self.inc_chan.shape), peak=False)
+        if not int(res.flags[0].item()) & N.FLAG_FEASIBLE:
+            raise ValueError("the incumbent structure is not feasible in explicit channel mode")
+        self.makespan = int(res.makespan[0].item())
+        self.initial_makespan = self.makespan
+        self.round = 0
+        self.evaluated = 0
+        self.improvements = []
+
+    @classmethod
+    def from_schedule(cls, inst, schedule, config: SearchConfig = SearchConfig(), device=None):
+        from .listsched import channel_order_of, stage_order_of
+        orders = {i: stage_order_of(schedule, i) for i in range(1, inst.num_stages + 1)}
+        chans = {g: channel_order_of(schedule, inst, g) for g in range(len(inst.topology_groups))}
+        return cls(inst, orders, schedule.offloaded, chans, config, device)
+
+    def _stream(self):
+        import torch
+        return C.c_void_p(torch.cuda.current_stream(self.di.device).cuda_stream)
+
+    def launch_round(self, makespan_out=None, first=0, count=None):
+        count = self.cfg.neighbours if count is None else count
+        self.best_key.fill_(N.BEST_NONE)
+        desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round, first, count,
+                            self.moves, None, None, 0)
+        N.check(self.lib.ps_search_round_explicit(
+            self.di.handle, C.byref(desc), C.c_void_p(self.inc_chan.data_ptr()), self.chan_stride,
+            C.c_void_p(self.best_key.data_ptr()),
+            C.c_void_p(makespan_out.data_ptr()) if makespan_out is not None else None, self._stream()))
+
+    def step(self, t0=None) -> bool:
+        self.launch_round()
+        key = int(self.best_key.item())
+        r = self.round
+        self.round += 1
+        self.evaluated += self.cfg.neighbours
+        if not improves(key, self.makespan):
+            return False
+        span, idx = unpack_key(key)
+        N.check(self.lib.ps_apply_move_explicit(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
+                                                C.c_void_p(self.inc_chan.data_ptr()), self.chan_stride,
+                                                C.byref(self.moves), r, idx, self._stream()))
+        self.makespan = span
+        self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
+        return True
+
+    def materialize(self, first: int, count: int, rnd: int | None = None):
+        import torch
+        pk = self.di.packed
+        dev = self.inc_orders.device
+        orders = torch.empty((count, pk.num_stages, pk.order_stride), dtype=torch.int16, device=dev)
+        masks = torch.empty((count, pk.mask_words), dtype=torch.int32, device=dev)
+        chans = torch.empty((count, pk.num_channels, self.chan_stride), dtype=torch.int32, device=dev)
+        desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(),
+                            self.round if rnd is None else rnd, first, count, self.moves)
+        N.check(self.lib.ps_materialize_moves_explicit(
+            self.di.handle, C.byref(desc), C.c_void_p(self.inc_chan.data_ptr()), self.chan_stride,
+            C.c_void_p(orders.data_ptr()), C.c_void_p(masks.data_ptr()), C.c_void_p(chans.data_ptr()),
+            self._stream()))
+        return orders, masks, chans
+
+    def incumbent_structure(self):
+        """(stage orders, offloaded set, channel orders) of the incumbent."""
+        from .packing import decode_mask, decode_orders
+        from .schedule import TransferKind
+        from .instance import OpId, OpKind
+        pk = self.di.packed
+        ch = self.inc_chan.cpu().numpy().view(np.uint32)
+        chans = {}
+        for g in range(pk.num_channels):
+            seq = []
+            for e in ch[g]:
+                if int(e) == 0xFFFFFFFF:
+                    break
+                e = int(e)
+                seq.append((OpId(((e >> 16) & 0x7FFF) + 1, (e & 0xFFFF) + 1, OpKind.F),
+                            TransferKind.RELOAD if e >> 31 else TransferKind.OFFLOAD))
+            chans[g] = tuple(seq)
+        return (decode_orders(pk, self.inc_orders.cpu().numpy().view(np.uint16)),
+                decode_mask(pk, self.inc_mask.cpu().numpy().view(np.uint32)), chans)
+
+    def run(self, rounds: int | None = None, time_budget: float | None = None,
+            patience: int | None = None) -> SearchResult:
+        from .listsched import run_order
+        if rounds is None and time_budget is None and patience is None:
+            raise ValueError("need rounds, time_budget or patience")
+        t0 = time.perf_counter()
+        stale = 0
+        while True:
+            if rounds is not None and self.round >= rounds:
+                break
+            if time_budget is not None and time.perf_counter() - t0 >= time_budget:
+                break
+            if self.step(t0):
+                stale = 0
+            else:
+                stale += 1
+                if patience is not None and stale >= patience:
+                    break
+        orders, off, chans = self.incumbent_structure()
+        sched = run_order(self.inst, orders, off, chans, device=self.di.device)
+        return SearchResult(sched, self.makespan, self.initial_makespan, self.round, self.evaluated,
+                            time.perf_counter() - t0, list(self.improvements))

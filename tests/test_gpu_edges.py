@@ -172,3 +172,30 @@ def test_malformed_rows_match_the_reference(cuda_ok, explicit):
             assert list(err.value.stages) == case["infeasible"]
             n += 1
     assert n >= (20 if explicit else 150)
+
+
+def test_delta_encoded_host_batch_equals_the_full_rows(cuda_ok):
+    """ps_eval_batch_host_delta (candidates as differences from a reference structure, only the
+    differences cross PCIe) gives the same outputs as ps_eval_batch_host on the full rows, with
+    and without a recorded base, config 2 (m <= 64) and config 4 (m > 64)."""
+    import torch
+    from paper_2510_05186_b200.engine import Base
+    from paper_2510_05186_b200.packing import delta_encode
+    for cfg in (2, 4):
+        inst, pk, base, di = _setup(cfg)
+        rng = np.random.default_rng(cfg)
+        o0, mk0, _ = base[-1]
+        orders, masks, kinds = _malformed_batch(pk, [(o0, mk0, None)], rng)
+        keep = [k for k, kind in enumerate(kinds) if kind in (0, 1, 4)]      # codes that name ops
+        orders, masks = orders[keep], masks[keep]
+        b = Base(di)
+        b.record(torch.from_numpy(o0.view(np.int16)).cuda(), torch.from_numpy(mk0.view(np.int32)).cuda())
+        enc = delta_encode(o0, mk0, orders, masks)
+        assert int(enc[0][-1]) < orders.size // 4          # far fewer entries than the full rows
+        for bb in (None, b):
+            want = di.evaluate_host(orders, masks, peak=True, base=bb)
+            got = di.evaluate_host_delta(o0, mk0, *enc, peak=True, base=bb)
+            for f in ("flags", "makespan", "peak", "blocked"):
+                assert (getattr(got, f) == getattr(want, f)).all(), (cfg, f)
+            ok = want.flags == 1
+            assert (got.bubble[ok] == want.bubble[ok]).all()

@@ -386,3 +386,106 @@ def test_iterated_local_search_follows_the_cpu_restatement(cuda_ok):
     assert (ls.best_mask.cpu().numpy().view(np.uint32) == want["best_mask"]).all()
     from paper_2510_05186_b200 import makespan, validate
     assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == res.makespan
+
+
+def _channel_search(n=512):
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.search import ChannelSearch, SearchConfig
+    inst = workloads.config2()
+    s, _ = best_feasible(inst)
+    cs = ChannelSearch.from_schedule(inst, s, SearchConfig(seed=SEED, neighbours=n, shift_permille=400,
+                                                           max_shift=MAXSHIFT))
+    return inst, s, cs
+
+
+def test_channel_search_moves_match_the_cpu_restatement(cuda_ok):
+    """Channel-order neighbours (stage-op shifts and transfer shifts within a channel, DESIGN.md
+    §4.2) decoded on the device equal or_neighbour_explicit's, and the explicit replay of the warm
+    schedule's channel orders reproduces its makespan."""
+    from oracle.oracle import Oracle, neighbour_explicit
+    from paper_2510_05186_b200 import makespan
+    inst, s, cs = _channel_search()
+    assert cs.makespan == makespan(s, inst)
+    orc = Oracle(cs.di.packed)
+    inc_o = cs.inc_orders.cpu().numpy().view(np.uint16)
+    inc_m = cs.inc_mask.cpu().numpy().view(np.uint32)
+    inc_c = cs.inc_chan.cpu().numpy().view(np.uint32)
+    kinds = set()
+    for rnd in (0, 7):
+        o, mk, ch = cs.materialize(0, 512, rnd)
+        o, mk, ch = (t.cpu().numpy().view(dt) for t, dt in ((o, np.uint16), (mk, np.uint32), (ch, np.uint32)))
+        for idx in range(512):
+            t, oo, mm, cc = neighbour_explicit(orc, inc_o, inc_m, inc_c, SEED, 400, MAXSHIFT, rnd, idx)
+            kinds.add(t)
+            assert (oo == o[idx]).all() and (mm == mk[idx]).all() and (cc == ch[idx]).all(), (rnd, idx, t)
+    assert kinds == {0, 1, 3}
+
+
+def test_channel_search_rounds_and_trail_match_the_cpu_restatement(cuda_ok):
+    import torch
+    from oracle.oracle import Oracle, search_round_explicit
+    inst, s, cs = _channel_search(n=1024)
+    orc = Oracle(cs.di.packed)
+    inc_o = cs.inc_orders.cpu().numpy().view(np.uint16)
+    inc_m = cs.inc_mask.cpu().numpy().view(np.uint32)
+    inc_c = cs.inc_chan.cpu().numpy().view(np.uint32)
+    ms = torch.empty(1024, dtype=torch.int64, device="cuda")
+    cs.launch_round(ms)
+    best, want = search_round_explicit(orc, inc_o, inc_m, inc_c, SEED, 400, MAXSHIFT, 0, 0, 1024, want_makespans=True)
+    assert (ms.cpu().numpy() == want).all()
+    assert int(cs.best_key.item()) == best
+    # a whole search: same adopted moves as the CPU restatement
+    from oracle.oracle import neighbour_explicit
+    span, trail = cs.makespan, []
+    for rnd in range(6):
+        b, _ = search_round_explicit(orc, inc_o, inc_m, inc_c, SEED, 400, MAXSHIFT, rnd, 0, 1024)
+        if b != (1 << 63) - 1 and (b >> 32) < span:
+            span = b >> 32
+            _, inc_o, inc_m, inc_c = neighbour_explicit(orc, inc_o, inc_m, inc_c, SEED, 400, MAXSHIFT, rnd,
+                                                        b & 0xFFFFFFFF)
+            trail.append((rnd, span))
+    res = cs.run(rounds=6)
+    assert [(i.round, i.makespan) for i in res.improvements] == trail and len(trail) > 0
+    assert (cs.inc_chan.cpu().numpy().view(np.uint32) == inc_c).all()
+    from paper_2510_05186_b200 import makespan, validate
+    assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == span
+
+
+@pytest.mark.parametrize("late", [False, True])
+def test_bound_pruning_keeps_every_round_decision(cuda_ok, late):
+    """Search rounds with the incumbent's makespan as cutoff abandon neighbours
+    whose bound reaches it; a round's adopted move (a strict improvement) is the same as with every
+    neighbour simulated — config 3, from the warm start and from the late incumbent."""
+    import ctypes as C
+    import torch
+    from paper_2510_05186_b200 import _native as N
+    from paper_2510_05186_b200.search import improves
+    inst, orders, off, LocalSearch, SearchConfig = _setup(3)
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=65536))
+    if late:
+        z = np.load(Path(__file__).parent / "golden" / "inc320_config3.npz")
+        ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
+        ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
+        ls.base.record(ls.inc_orders, ls.inc_mask)
+        r = ls.di.evaluate(ls.inc_orders.view(1, *ls.inc_orders.shape), ls.inc_mask.view(1, -1), peak=False)
+        ls.makespan = int(r.makespan[0].item())
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    adopted = 0
+    for rnd in range(6):
+        keys = []
+        for cutoff in (0, ls.makespan):
+            k = torch.full((1,), N.BEST_NONE, dtype=torch.int64, device="cuda")
+            desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, 65536, ls.moves, None,
+                                ls.base.handle, 1, cutoff)
+            N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(k.data_ptr()), None, stream))
+            keys.append(int(k.item()))
+        full, pruned = keys
+        assert improves(full, ls.makespan) == improves(pruned, ls.makespan), rnd
+        if improves(full, ls.makespan):
+            assert full == pruned
+            adopted += 1
+            ls.best_key.fill_(full)
+            ls.round = rnd
+            ls.finish_round()
+    assert adopted >= 1 or late

@@ -104,3 +104,31 @@ def test_bound_restatement_matches_reference_solver():
             assert bound(orc, node["t"], node["sfree"], st, r["post"]) == node["lb"]
             n += 1
     assert n > 5000
+
+
+def test_channel_neighbours_restate_the_stage_shift_and_keep_channel_lengths():
+    """or_neighbour_explicit: with shift_permille 1000 it is or_neighbour's stage
+    shift; its transfer shifts permute one channel's entries and never change the offload bits."""
+    import numpy as np
+    from oracle.oracle import Oracle, neighbour_explicit
+    from _golden import case_arrays, corpus
+    for inst, pk, cases in corpus("ref_tests"):
+        sel = [c for c in cases if "channel_orders" in c and "makespan" in c and any(c["channel_orders"])]
+        if not sel:
+            continue
+        orc = Oracle(pk)
+        o, mk, ch = case_arrays(pk, sel[0])
+        seen = set()
+        for idx in range(64):
+            t0, o0, m0 = orc.neighbour(o, mk, 5, 700, 4, 3, idx)
+            t1, o1, m1, c1 = neighbour_explicit(orc, o, mk, ch, 5, 1000, 4, 3, idx)
+            if t0 == 1:
+                assert t1 == 1 and (o1 == o0).all()
+            t2, o2, m2, c2 = neighbour_explicit(orc, o, mk, ch, 5, 0, 4, 3, idx)
+            seen.add(t2)
+            assert (m2 == mk).all() and (o2 == o).all()
+            for g in range(ch.shape[0]):
+                assert sorted(c2[g].tolist()) == sorted(ch[g].tolist())
+        assert 3 in seen
+        return
+    raise AssertionError("no explicit-mode fixture with transfers")

@@ -112,5 +112,32 @@ def ils(inst, seed, neighbours, kick_moves, budget_s, device=0):
     return best, it, trace
 
 
+def channel_polish(cfg=2, ils_seconds=5.0, neighbours=4096):
+    """ILS for ils_seconds, then the channel-order search (reload/offload shifts)
+    from its best schedule until 16 rounds bring nothing: does reordering transfers help?"""
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200.search import ChannelSearch, LocalSearch, SearchConfig
+    inst = workloads.CONFIGS[cfg]()
+    s0, _ = best_feasible(inst, device=0)
+    orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
+    ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=1, neighbours=neighbours, kick_moves=4), device=0)
+    res = ls.run(time_budget=ils_seconds)
+    out = {"config": cfg, "ils_best": res.makespan}
+    for permille in (0, 300):
+        cs = ChannelSearch.from_schedule(inst, res.schedule, SearchConfig(seed=2, neighbours=neighbours,
+                                                                          shift_permille=permille), device=0)
+        t0 = time.perf_counter()
+        r2 = cs.run(patience=16)
+        out[f"channel_{permille}"] = {"best": r2.makespan, "rounds": cs.round, "seconds": time.perf_counter() - t0,
+                                      "improvements": len(r2.improvements)}
+    print(json.dumps(out), flush=True)
+
+
 if __name__ == "__main__":
-    main_ils() if "--ils" in sys.argv else main()
+    if "--channel" in sys.argv:
+        for c in (2, 3):
+            channel_polish(c, 5.0, 4096 if c == 2 else 65536)
+    else:
+        main_ils() if "--ils" in sys.argv else main()
