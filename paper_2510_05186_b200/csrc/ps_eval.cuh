@@ -159,6 +159,61 @@ __device__ __forceinline__ void warp_copy_words_mlp(uint32_t *dst, const uint32_
     for (int q = (n4 << 2) + lane; q < n; q += 32) dst[q] = src[q];
 }
 
+// Any-alignment warp copy/zero: 16-byte vectors when both ends allow, words otherwise.
+__device__ __forceinline__ void warp_copy_words_any(uint32_t *dst, const uint32_t *src, int n, int lane) {
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u) == 0) {
+        warp_copy_words(dst, src, n, lane);
+        return;
+    }
+#pragma unroll 1
+    for (int k = lane; k < n; k += 32) dst[k] = src[k];
+}
+__device__ __forceinline__ void warp_zero_words_any(uint32_t *dst, int n, int lane) {
+    if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        warp_zero_words(dst, n, lane);
+        return;
+    }
+#pragma unroll 1
+    for (int k = lane; k < n; k += 32) dst[k] = 0u;
+}
+// One lane's copy of words [lo, hi) of a row (band restore): with `vec`, the range
+// widened to 16-byte boundaries (the caller guarantees the widened words are equal on both sides
+// or irrelevant) and U vector loads in flight.
+template <int U>
+__device__ __forceinline__ void lane_copy_range(uint32_t *dst, const uint32_t *src, int lo, int hi, bool vec) {
+    if (lo >= hi) return;
+    if (vec) {
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        int k = lo >> 2;
+        const int e = (hi + 3) >> 2;
+#pragma unroll 1
+        for (; k + U <= e; k += U) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = s4[k + u];
+#pragma unroll
+            for (int u = 0; u < U; ++u) d4[k + u] = v[u];
+        }
+#pragma unroll 1
+        for (; k < e; ++k) d4[k] = s4[k];
+        return;
+    }
+#pragma unroll 1
+    for (int k = lo; k < hi; ++k) dst[k] = src[k];
+}
+__device__ __forceinline__ void lane_zero_range(uint32_t *dst, int lo, int hi, bool vec) {
+    if (lo >= hi) return;
+    if (vec) {
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+#pragma unroll 1
+        for (int k = lo >> 2; k < (hi + 3) >> 2; ++k) d4[k] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
+#pragma unroll 1
+    for (int k = lo; k < hi; ++k) dst[k] = 0u;
+}
+
 __device__ __forceinline__ unsigned long long make_key(uint32_t hi, uint32_t lo) {
     return ((unsigned long long)hi << 32) | lo;
 }
@@ -316,6 +371,16 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     int wt = -1;        // see compute_key
     int lastq = -1;     // last position of this stage's order that differs from the base's
     int eoff = 0;       // base step = candidate step + eoff once the candidate's extra/missing transfers are done
+    // Row bands.  A stage's end-time rows are A_DEAD (A row) / zero (X row) below the
+    // band of microbatches in flight and zero above it, in the slot as in every checkpoint (whose band
+    // a recording saves in register word 21/22).  Global-state evaluation passes (BAND) therefore
+    // restore and compare only the rows' bands: this lane's A row is A_DEAD below b_alo, its X row
+    // zero below b_xlo, both zero from b_hi on (the slot starts unknown: everything is rewritten).
+    // A recording tracks the same bounds to save them.
+    constexpr bool BAND = GSTATE && !REC;
+    int b_alo = 0, b_xlo = 0, b_hi = m;
+    // 16-byte vectors over the rows: row starts and checkpoints on 16-byte boundaries
+    const bool band_vec = ((o_A | m | p.cand_words | p.ck_words) & 3) == 0;
 
     // op code idx of the staged candidate rows ([P][stride], uint8 or uint16)
     auto row_at = [&](int idx) -> uint32_t {
@@ -705,7 +770,64 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         // be irrelevant in the candidate too (dom_bound); state-only words must be equal
         const uint32_t d4 = (uint32_t)d << 2;
         const int n2 = 2 * P * m;
-        if (GSTATE && PS_GSTATE_VEC_CMP == 2) {
+        if constexpr (BAND) {
+            // Each lane compares its own stage's rows over the union of the two bands (outside it
+            // both sides are A_DEAD below and zero above), 16-byte vectors, two of each in flight.
+            // dom_bound's readers are this stage's neighbours: their free times are shuffled once.
+            const int sf_up = __shfl_sync(0xffffffffu, sfree, min(i + 1, 31));
+            const int sf_dn = __shfl_sync(0xffffffffu, sfree, max(i - 1, 0));
+            if (has_stage) {
+                while (b_alo < b_hi && SW(o_Ai + (b_alo)) == A_DEAD) ++b_alo;   // (monotone: amortised)
+                b_xlo = max(b_xlo, b_alo);                                    // A_DEAD => X word zero
+                const int hi = max(b_hi, (int)rg[22]);
+                auto word_ok = [&](bool isA, int j, uint32_t cw, uint32_t bw) -> bool {
+                    const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
+                    if (timed_c == timed_b && (timed_c ? cw - bw == d4 : cw == bw)) return true;
+                    if (!(timed_c && !timed_b && (cw & 3u) == bw)) return false;
+                    int bound = INT_MAX;                  // dom_bound for a word of this lane's rows
+                    const uint32_t st = cw & 3u;
+                    if (isA && st == 1u) {
+                        if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
+                        if (((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) && (SW(o_Xi + (j)) & 3u) == 0u)
+                            bound = min(bound, cfree);
+                    } else if (isA) {
+                        if (i > 0 && (SW(o_A + ((i - 1) * m + j)) & 3u) < 2u) bound = min(bound, sf_dn - p.comm);
+                    } else if (st == 2u) {
+                        bound = min(bound, sfree);
+                    }
+                    return bound != INT_MAX && (int)(cw >> 2) <= bound;
+                };
+                auto cmp_row = [&](bool isA, int row_off, const uint32_t *brow, int lo) -> bool {
+                    if (lo >= hi) return true;
+                    if (band_vec) {
+                        const uint4 *c4 = reinterpret_cast<const uint4 *>(&SW(row_off));
+                        const uint4 *b4 = reinterpret_cast<const uint4 *>(brow);
+                        const int e = (hi + 3) >> 2;
+#pragma unroll 1
+                        for (int k = lo >> 2; k < e; k += 2) {
+                            const bool two = k + 1 < e;
+                            const uint4 ca = c4[k], ba = b4[k];
+                            const uint4 cb = two ? c4[k + 1] : ca, bb = two ? b4[k + 1] : ba;
+                            const int j = 4 * k;
+                            if (!(word_ok(isA, j, ca.x, ba.x) && word_ok(isA, j + 1, ca.y, ba.y) &&
+                                  word_ok(isA, j + 2, ca.z, ba.z) && word_ok(isA, j + 3, ca.w, ba.w)))
+                                return false;
+                            if (two && !(word_ok(isA, j + 4, cb.x, bb.x) && word_ok(isA, j + 5, cb.y, bb.y) &&
+                                         word_ok(isA, j + 6, cb.z, bb.z) && word_ok(isA, j + 7, cb.w, bb.w)))
+                                return false;
+                        }
+                        return true;
+                    }
+#pragma unroll 1
+                    for (int j = lo; j < hi; ++j)
+                        if (!word_ok(isA, j, SW(row_off + j), brow[j])) return false;
+                    return true;
+                };
+                const int clo = (int)rg[21];
+                eq = cmp_row(true, o_Ai, src + i * m, min(b_alo, clo)) &&
+                     cmp_row(false, o_Xi, src + P * m + i * m, min(b_xlo, clo));
+            }
+        } else if (GSTATE && PS_GSTATE_VEC_CMP == 2) {
             // same test, PS_GSTATE_CMP_U coalesced rows of loads in flight before they are tested
             constexpr int U = PS_GSTATE_CMP_U;
             for (int k0 = 0; k0 < n2; k0 += 32 * U) {
@@ -821,7 +943,9 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             __syncwarp();
         }
         // ================= initialise ======================================================
-        warp_zero_words(&SW(o_A), nz, lane);
+        // (BAND: the rows are rewritten over their bands by the restore below; only the bitsets here)
+        if (BAND) warp_zero_words_any(&SW(o_A + 2 * P * m), nz - 2 * P * m, lane);
+        else warp_zero_words(&SW(o_A), nz, lane);
         if (!MOVES) {
             // stage the candidate's rows: 8-byte loads, coalesced across the warp
             const uint2 *src = reinterpret_cast<const uint2 *>(reinterpret_cast<const unsigned char *>(p.orders) +
@@ -917,6 +1041,10 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         if (k == 0u) fm |= bit; else if (k == 1u) bm |= bit; else wm |= bit;
                     }
                 } else {
+                    if (BAND) {            // the row is the seen-set scratch: clear it first
+                        lane_zero_range(&SW(o_Ai), 0, b_hi, band_vec);
+                        b_alo = 0;
+                    }
                     for (int q = 0; q < L; ++q) {
                         uint32_t op = row_at(i * p.stride + q);
                         uint32_t j = op >> 2, k = op & 3u;
@@ -1002,8 +1130,27 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 __syncwarp();
                 continue;
             }
-            if (GSTATE) warp_copy_words_mlp<PS_GSTATE_COPY_MLP>(&SW(o_A), src, nz, lane);
-            else warp_copy_words(&SW(o_A), src, nz, lane);
+            if (BAND) {
+                // the bitsets, then each stage's rows over the old and the checkpoint's band
+                warp_copy_words_any(&SW(o_A + 2 * P * m), src + 2 * P * m, nz - 2 * P * m, lane);
+                if (has_stage) {
+                    const uint32_t *rgs = src + ck_r + lane * CK_REGW;
+                    const int clo = (int)rgs[21], chi = (int)rgs[22];
+                    const int hi = max(b_hi, chi);
+                    lane_copy_range<4>(&SW(o_Ai), src + i * m, min(b_alo, clo), hi, band_vec);
+                    lane_copy_range<4>(&SW(o_Xi), src + P * m + i * m, min(b_xlo, clo), hi, band_vec);
+                    b_alo = b_xlo = clo;
+                    b_hi = chi;
+                }
+            } else if (GSTATE) {
+                warp_copy_words_mlp<PS_GSTATE_COPY_MLP>(&SW(o_A), src, nz, lane);
+            } else {
+                warp_copy_words(&SW(o_A), src, nz, lane);
+            }
+            if (REC && has_stage) {
+                b_alo = b_xlo = (int)src[ck_r + lane * CK_REGW + 21];
+                b_hi = (int)src[ck_r + lane * CK_REGW + 22];
+            }
             if (has_stage) {
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
@@ -1034,6 +1181,11 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             ecount0 = ecount;
             cc = ck_idx * p.ck_interval;
         } else {
+            if (BAND && has_stage) {
+                lane_zero_range(&SW(o_Ai), 0, b_hi, band_vec);
+                lane_zero_range(&SW(o_Xi), b_xlo, b_hi, band_vec);
+            }
+            b_alo = b_xlo = b_hi = 0;
             ecount0 = 0;
             pos = 0; sfree = 0; cfree = 0;
             base = top = peak = 0; ws = we = 0;
@@ -1137,6 +1289,12 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         we -= ws;
                         ws = 0;
                         uint32_t *rg = dst + ck_r + lane * CK_REGW;
+                        if (has_stage) {
+                            // the rows' band at this checkpoint (read by BAND restores and compares)
+                            while (b_alo < b_hi && SW(o_Ai + (b_alo)) == A_DEAD) ++b_alo;
+                            rg[21] = (uint32_t)b_alo;
+                            rg[22] = (uint32_t)b_hi;
+                        }
                         save_regs(rg);
                         *reinterpret_cast<long long *>(rg + 10) = (long long)segpk;
                         rg[9] = (uint32_t)max_win;     // widest window so far
@@ -1179,6 +1337,8 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                     // come; readers on the op's own stage are bounded by its free time, so there the
                     // time is dropped (canonical words).
                     if (k == KIND_F) {
+                        // (every later write to row i, or row i's X, at microbatch j follows this F)
+                        if (BAND || REC) b_hi = max(b_hi, j + 1);
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
                         if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
                         if (i > 0) {

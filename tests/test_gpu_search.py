@@ -194,6 +194,35 @@ def test_prefix_sharing_is_exact(cuda_ok, cfg):
     _eval_both(ls.di, o, mk, bad)
 
 
+@pytest.mark.parametrize("cfg,n", [(4, 16384), (5, 4096)])
+def test_global_state_row_bands_are_exact(cuda_ok, cfg, n):
+    """Configs 4 and 5 keep each warp's candidate state in global scratch and restore / compare only
+    the end-time rows' bands.  With several neighbours per warp (so each slot goes
+    through resumes from different checkpoints, fresh starts and convergences in turn), a search
+    round with the recorded base gives every neighbour the makespan of its full simulation."""
+    import ctypes as C
+    import torch
+    from paper_2510_05186_b200 import _native as N
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    got = []
+    for rnd in (0, 1):
+        for base in (ls.base, None):
+            out = torch.empty(n, dtype=torch.int64, device="cuda")
+            ls.best_key.fill_(N.BEST_NONE)
+            desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, n, ls.moves, None,
+                                base.handle if base is not None else None)
+            N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
+                                           C.c_void_p(out.data_ptr()), ls._stream()))
+            torch.cuda.synchronize()
+            got.append((out.cpu().numpy(), int(ls.best_key.item())))
+        (a, ka), (b, kb) = got[-2], got[-1]
+        assert (a == b).all(), (rnd, int((a != b).sum()))
+        assert ka == kb
+        assert (a >= 0).any()
+
+
 @pytest.mark.parametrize("cfg", [2, 3])
 def test_rerecorded_base_is_exact(cuda_ok, cfg):
     """A base re-recorded over a previous one (it resumes from the previous checkpoints up to their
