@@ -237,7 +237,8 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
         pl->gstate = true;
         pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
-        pl->cfg.smem = (size_t)pl->inc_words * 4;
+        // behind it, each warp's offload / pending-transfer bitsets (read on most events)
+        pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * ((3 * I->P * I->MW + 3) & ~3)) * 4;
         pl->cfg.block = 32 * pl->warps;
     };
     int per_sm = 0, rc;

@@ -310,10 +310,17 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     const int o_A = P * 2 * K * (VW + 1);                       // [P][m] F end, then B end (time<<2 | state)
     const int o_Ai = o_A + is * m;
     const int o_Xi = o_A + P * m + is * m;                      // [P][m] offload end, then reload end
-    const int o_offm = o_A + 2 * P * m + is * MW;               // [P][MW] offloaded bits
+    // Per-stage bitsets [3][P][MW] (offloaded, pending offloads, pending reloads), addressed by SB()
+    // relative to their start: after the rows in the state block, or (global-state passes) in the
+    // warp's slice of shared memory behind the incumbent, where the event loop's many reads of them
+    // stay on chip (checkpoints keep them after the rows either way).
+    const int o_offm = is * MW;                                 // [P][MW] offloaded bits
     const int o_poff = o_offm + P * MW;                         // [P][MW] pending offload requests
     const int o_prel = o_poff + P * MW;                         // [P][MW] pending reload requests
-    const int nz = 2 * P * m + 3 * P * MW;               // words zeroed per candidate
+    const int nb3 = 3 * P * MW;                                 // bitset words
+    const int nz = 2 * P * m + nb3;                      // words zeroed per candidate
+    const int sbits = p.inc_words + warp * ((nb3 + 3) & ~3);    // (global state) shared-memory bitsets
+#define SB(off) (GSTATE ? smem[sbits + (off)] : smem[sbase + o_A + 2 * P * m + (off)])
     // materialised candidates: the candidate's stage orders, staged once (8-byte aligned)
     const int o_row = o_A + ((nz + 1) & ~1);
     const int row_bytes = P * p.stride * (p.order_u8 ? 1 : 2);
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 if ((b & 3u) < 2u) { wt = i + 1; return; }   // 2: B committed, 3: and W too
                 fl = max(fl, (int)(b >> 2) + p.comm);
             }
-            if ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) {
+            if ((SB(o_offm + (j >> 5)) >> (j & 31)) & 1u) {
                 uint32_t x = SW(o_Xi + (j));
                 if ((x & 3u) != 2u) return;
                 fl = max(fl, (int)(x >> 2));
@@ -571,14 +578,14 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         if (derived) {
             if (n_poff)
                 for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = SW(o_poff + (w)); bits; bits &= bits - 1) {
+                    for (uint32_t bits = SB(o_poff + (w)); bits; bits &= bits - 1) {
                         int j = w * 32 + __ffs(bits) - 1;
                         best = min(best, make_key((uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C),
                                                   (2u << 30) | stb | ((uint32_t)j << 2)));
                     }
             if (n_prel)
                 for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = SW(o_prel + (w)); bits; bits &= bits - 1) {
+                    for (uint32_t bits = SB(o_prel + (w)); bits; bits &= bits - 1) {
                         int j = w * 32 + __ffs(bits) - 1;
                         int tau = tau_G(limit_i - val_of(j, 3));
                         if (tau == TAU_NONE) continue;
@@ -662,7 +669,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     // is dead once that microbatch's B has committed on this stage.
     auto diff_dead = [&]() -> bool {
         for (int w = 0; w < MW; ++w)
-            for (uint32_t x = SW(o_offm + (w)) ^ base_word(w); x; x &= x - 1)
+            for (uint32_t x = SB(o_offm + (w)) ^ base_word(w); x; x &= x - 1)
                 if ((SW(o_Ai + (w * 32 + __ffs(x) - 1)) & 3u) < 2u) return false;
         return true;
     };
@@ -683,7 +690,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             const uint32_t st = w & 3u;
             if (isA && st == 1u) {          // F end: F(si+1, j), and F(si, j)'s offload
                 if (si + 1 < P && (SW(o_A + ((si + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
-                if (((SW(o_A + (2 * P * m + si * MW + (j >> 5))) >> (j & 31)) & 1u) &&
+                if (((SB(si * MW + (j >> 5)) >> (j & 31)) & 1u) &&
                     (SW(o_A + (P * m + si * m + j)) & 3u) == 0u)
                     bound = min(bound, cf_own);
             } else if (isA) {               // B end: B(si-1, j)
@@ -788,7 +795,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                     const uint32_t st = cw & 3u;
                     if (isA && st == 1u) {
                         if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
-                        if (((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u) && (SW(o_Xi + (j)) & 3u) == 0u)
+                        if (((SB(o_offm + (j >> 5)) >> (j & 31)) & 1u) && (SW(o_Xi + (j)) & 3u) == 0u)
                             bound = min(bound, cfree);
                     } else if (isA) {
                         if (i > 0 && (SW(o_A + ((i - 1) * m + j)) & 3u) < 2u) bound = min(bound, sf_dn - p.comm);
@@ -899,8 +906,8 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
 #ifdef PS_DEBUG_CONV
         if (!__all_sync(0xffffffffu, eq)) { dbg(7); return false; }
 #endif
-        PS_NOUNROLL_C for (int k = 2 * P * m + P * MW + lane; k < nz; k += 32)     // (offm skipped: its differences are dead)
-            eq = eq && SW(o_A + (k)) == src[k];
+        PS_NOUNROLL_C for (int k = P * MW + lane; k < nb3; k += 32)     // (offm skipped: its differences are dead)
+            eq = eq && SB(k) == src[2 * P * m + k];
 #ifdef PS_DEBUG_CONV
         if (!__all_sync(0xffffffffu, eq)) { dbg(8); return false; }
 #endif
@@ -944,7 +951,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         }
         // ================= initialise ======================================================
         // (BAND: the rows are rewritten over their bands by the restore below; only the bitsets here)
-        if (BAND) warp_zero_words_any(&SW(o_A + 2 * P * m), nz - 2 * P * m, lane);
+        if (BAND) warp_zero_words_any(&SB(0), nb3, lane);
         else warp_zero_words(&SW(o_A), nz, lane);
         if (!MOVES) {
             // stage the candidate's rows: 8-byte loads, coalesced across the warp
@@ -976,7 +983,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 const int nb = m - w * 32;
                 if (nb < 32) bits &= (1u << nb) - 1u;
                 if (MOVES && mv.type == MOVE_TOGGLE && mv.stage == i && (mv.mb >> 5) == w) bits ^= 1u << (mv.mb & 31);
-                SW(o_offm + (w)) = bits;
+                SB(o_offm + (w)) = bits;
                 n += __popc(bits);
                 // an offload bit on a non-offloadable op is malformed (KeyError in the reference)
                 if (check)
@@ -1091,7 +1098,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                     for (int w = 0; w < MW; ++w) {
                         const uint32_t bb = base_word(w);
                         nbase += __popc(bb);
-                        for (uint32_t x = SW(o_offm + (w)) ^ bb; x; x &= x - 1)
+                        for (uint32_t x = SB(o_offm + (w)) ^ bb; x; x &= x - 1)
                             d = min(d, p.fstep[i * m + w * 32 + __ffs(x) - 1]);
                     }
                 }
@@ -1132,7 +1139,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             }
             if (BAND) {
                 // the bitsets, then each stage's rows over the old and the checkpoint's band
-                warp_copy_words_any(&SW(o_A + 2 * P * m), src + 2 * P * m, nz - 2 * P * m, lane);
+                warp_copy_words_any(&SB(0), src + 2 * P * m, nb3, lane);
                 if (has_stage) {
                     const uint32_t *rgs = src + ck_r + lane * CK_REGW;
                     const int clo = (int)rgs[21], chi = (int)rgs[22];
@@ -1163,7 +1170,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 // this candidate's offload bits: any difference lies on an F the base has not
                 // committed yet, so only the outstanding-transfer count moves
                 int nb = 0;
-                for (int w = 0; w < MW; ++w) nb += __popc(SW(o_offm + (w)));
+                for (int w = 0; w < MW; ++w) nb += __popc(SB(o_offm + (w)));
                 n_unrel += cand_unrel - nb;
                 build_mask(false);
                 if (REC) {
@@ -1172,7 +1179,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                     // reads both)
                     for (int c = 0; c <= ck_idx; ++c) {
                         uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                        for (int w = 0; w < MW; ++w) dst[2 * P * m + i * MW + w] = SW(o_offm + (w));
+                        for (int w = 0; w < MW; ++w) dst[2 * P * m + i * MW + w] = SB(o_offm + (w));
                         dst[ck_r + lane * CK_REGW + 7] += (uint32_t)(cand_unrel - nb);
                     }
                 }
@@ -1326,7 +1333,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 if (i == w) {
                     const int end = t + proc_of(j, k);
                     rem -= end - t;
-                    const bool newreq = derived && k == KIND_F && ((SW(o_offm + (j >> 5)) >> (j & 31)) & 1u);
+                    const bool newreq = derived && k == KIND_F && ((SB(o_offm + (j >> 5)) >> (j & 31)) & 1u);
                     win_insert(end, val_of(j, k));
                     sfree = end;
                     ++pos;
@@ -1340,11 +1347,11 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         // (every later write to row i, or row i's X, at microbatch j follows this F)
                         if (BAND || REC) b_hi = max(b_hi, j + 1);
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
-                        if (newreq) { SW(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
+                        if (newreq) { SB(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
                         if (i > 0) {
                             // F(i, j) read A[i-1][j]; unless F(i-1, j)'s offload is still to come,
                             // only B(i-1, j) reads it now
-                            const bool off_pending = ((SW(o_A + (2 * P * m + (i - 1) * MW + (j >> 5))) >> (j & 31)) & 1u) &&
+                            const bool off_pending = ((SB((i - 1) * MW + (j >> 5)) >> (j & 31)) & 1u) &&
                                                      (SW(o_A + (P * m + (i - 1) * m + j)) & 3u) == 0u;
                             if (!off_pending) SW(o_A + ((i - 1) * m + j)) = 1u;
                         }
@@ -1382,12 +1389,12 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         SW(o_Xi + (j)) = 1u;
                         if (i == P - 1 || (SW(o_A + ((i + 1) * m + j)) & 3u) != 0u) SW(o_Ai + (j)) = 1u;
                         win_insert(end, -g);
-                        if (derived) { SW(o_poff + (j >> 5)) &= ~bit; SW(o_prel + (j >> 5)) |= bit; --n_poff; ++n_prel; }
+                        if (derived) { SB(o_poff + (j >> 5)) &= ~bit; SB(o_prel + (j >> 5)) |= bit; --n_poff; ++n_prel; }
                     } else {
                         SW(o_Xi + (j)) = ((uint32_t)end << 2) | 2u;
                         win_insert(t, g);
                         --n_unrel;
-                        if (derived) { SW(o_prel + (j >> 5)) &= ~bit; --n_prel; }
+                        if (derived) { SB(o_prel + (j >> 5)) &= ~bit; --n_prel; }
                     }
                     // the ledger changed: an F head re-fits; a B head may have been waiting on this reload
                     cdirty = cdirty || (pos < L && ((head & 3u) == KIND_F || head == (((uint32_t)j << 2) | KIND_B)));
@@ -1575,6 +1582,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     }
 #undef SW
 #undef SV
+#undef SB
 }
 
 }  // namespace ps
