@@ -134,6 +134,7 @@ int next_pow2(int x) {
 struct Plan {
     int K, warps;
     bool gstate;
+    bool win_smem;      // global state: the ledger windows in shared memory
     int cand_words, inc_words;
     LaunchCfg cfg;
     size_t scratch_bytes;
@@ -189,6 +190,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
     pl->cand_words = words_per_candidate(I, K, moves ? 0 : order_bytes);
     pl->inc_words = incumbent_words(I, moves);
     pl->gstate = true;
+    pl->win_smem = false;
     pl->warps = 4;
     const int max_warps = std::max(1, std::min(4, env_int("PS_WARPS_PER_BLOCK", 4)));
     const bool force_g = env_int("PS_FORCE_GSTATE", 0) != 0;     // (experiments)
@@ -239,6 +241,11 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
         // behind it, each warp's offload / pending-transfer bitsets (read on most events)
         pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * ((3 * I->P * I->MW + 3) & ~3)) * 4;
+        // and, when they fit, their ledger windows (the event loop's other hot words)
+        const size_t win = (size_t)pl->warps * I->P * 2 * pl->K * ((I->v64 ? 2 : 1) + 1) * 4;
+        pl->win_smem = env_int("PS_WIN_SMEM", 1) != 0 &&
+                       pl->cfg.smem + win <= (size_t)env_int("PS_WIN_SMEM_MAX", I->max_smem_optin);
+        if (pl->win_smem) pl->cfg.smem += win;
         pl->cfg.block = 32 * pl->warps;
     };
     int per_sm = 0, rc;
@@ -341,6 +348,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.K = pl.K;
         q.cand_words = pl.cand_words;
         q.inc_words = pl.inc_words;
+        q.win_smem = pl.gstate && pl.win_smem;
         int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order;         // handoff k-1
         int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
         q.work_count = in;

@@ -82,6 +82,7 @@ struct EvalParams {
     const int32_t *ready;
     long long ready_chunk;
     int dedup;               // (host side) evaluate each distinct move of a round once
+    int win_smem;            // global-state passes: the ledger windows live in shared memory
     long long cutoff;        // > 0: abandon a neighbour whose makespan bound reaches it (§3.13)
     const int32_t *work_list;
     const int32_t *work_count;
@@ -321,6 +322,13 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     const int nz = 2 * P * m + nb3;                      // words zeroed per candidate
     const int sbits = p.inc_words + warp * ((nb3 + 3) & ~3);    // (global state) shared-memory bitsets
 #define SB(off) (GSTATE ? smem[sbits + (off)] : smem[sbase + o_A + 2 * P * m + (off)])
+    // Ledger windows (offsets o_wu / o_wt from the state start): with win_smem, a global-state pass
+    // keeps them in the warp's shared-memory slice behind all warps' bitsets (same layout).
+    uint32_t *const wsw = !GSTATE ? nullptr
+                        : p.win_smem ? smem + p.inc_words + nwarps * ((nb3 + 3) & ~3) + warp * (P * 2 * K * (VW + 1))
+                                     : gsw;
+#define SWW(off) (GSTATE ? wsw[(off)] : smem[sbase + (off)])
+#define SVW(off) (GSTATE ? reinterpret_cast<V *>(wsw)[(off)] : reinterpret_cast<V *>(smem)[sbase / VW + (off)])
     // materialised candidates: the candidate's stage orders, staged once (8-byte aligned)
     const int o_row = o_A + ((nz + 1) & ~1);
     const int row_bytes = P * p.stride * (p.order_u8 ? 1 : 2);
@@ -438,12 +446,12 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     // base = usage at the fold line (the last folded breakpoint's), top = usage after everything.
     auto win_fold = [&](int line) {
         PS_HOT_LOOP(while (ws < we && wlo < line) {
-            V u = SV(o_wu + (ws));
+            V u = SVW(o_wu + (ws));
             peak = u > peak ? u : peak;
             if (REC) segpk = u > segpk ? u : segpk;
             base = u;
             ++ws;
-            wlo = ws < we ? (int)SW(o_wt + (ws)) : INT_MAX;
+            wlo = ws < we ? (int)SWW(o_wt + (ws)) : INT_MAX;
         })
         if (ws == we) whi = INT_MIN;
     };
@@ -458,26 +466,26 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         rF = rG = NO_R;                                // the ledger changed: drop cached answers
         int k = we - 1;
         if (ws < we && t == whi) {                     // same time as the last breakpoint: merge
-            SV(o_wu + (k)) += d;
+            SVW(o_wu + (k)) += d;
             return;
         }
         if (ws < we && t < whi) {
-            PS_HOT_LOOP(while (k >= ws && (int)SW(o_wt + (k)) > t) --k;)  // last breakpoint at or before t
-            if (k >= ws && (int)SW(o_wt + (k)) == t) {          // same time: merge into that breakpoint
-                PS_HOT_LOOP(for (int q = k; q < we; ++q) SV(o_wu + (q)) += d;)
+            PS_HOT_LOOP(while (k >= ws && (int)SWW(o_wt + (k)) > t) --k;)  // last breakpoint at or before t
+            if (k >= ws && (int)SWW(o_wt + (k)) == t) {          // same time: merge into that breakpoint
+                PS_HOT_LOOP(for (int q = k; q < we; ++q) SVW(o_wu + (q)) += d;)
                 return;
             }
         }
         if (we - ws == K) { ovf = true; return; }
         if (we == 2 * K) {                             // compact to the front
-            PS_HOT_LOOP(for (int q = ws; q < we; ++q) { SW(o_wt + (q - ws)) = SW(o_wt + (q)); SV(o_wu + (q - ws)) = SV(o_wu + (q)); })
+            PS_HOT_LOOP(for (int q = ws; q < we; ++q) { SWW(o_wt + (q - ws)) = SWW(o_wt + (q)); SVW(o_wu + (q - ws)) = SVW(o_wu + (q)); })
             k -= ws;
             we -= ws;
             ws = 0;
         }
-        PS_HOT_LOOP(for (int q = we - 1; q > k; --q) { SW(o_wt + (q + 1)) = SW(o_wt + (q)); SV(o_wu + (q + 1)) = SV(o_wu + (q)) + d; })
-        SW(o_wt + (k + 1)) = (uint32_t)t;
-        SV(o_wu + (k + 1)) = (k >= ws ? SV(o_wu + (k)) : base) + d;
+        PS_HOT_LOOP(for (int q = we - 1; q > k; --q) { SWW(o_wt + (q + 1)) = SWW(o_wt + (q)); SVW(o_wu + (q + 1)) = SVW(o_wu + (q)) + d; })
+        SWW(o_wt + (k + 1)) = (uint32_t)t;
+        SVW(o_wu + (k + 1)) = (k >= ws ? SVW(o_wu + (k)) : base) + d;
         ++we;
         if (k + 1 == we - 1) whi = t;                  // appended
         if (k + 1 == ws) wlo = t;                      // new first breakpoint
@@ -486,22 +494,22 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     auto win_tau = [&](V R) -> int {
         if (R < 0 || top > R) return TAU_NONE;
         int k = we - 1;
-        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > R)) --k;)
-        if (k >= ws) return (int)SW(o_wt + (k + 1));
-        return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
+        PS_HOT_LOOP(while (k >= ws && !(SVW(o_wu + (k)) > R)) --k;)
+        if (k >= ws) return (int)SWW(o_wt + (k + 1));
+        return base > R && ws < we ? (int)SWW(o_wt + (ws)) : TAU_ANY;
     };
     // Symmetric tables: the F and reload thresholds are per-stage constants with R_G >= R_F, so one
     // backward scan finds the last breakpoint above R_F and, continuing, the last above R_G.
     auto tau_pair = [&]() {
         const V RF = limit_i - v0, RG = limit_i - v3;
         int k = we - 1;
-        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > RF)) --k;)
+        PS_HOT_LOOP(while (k >= ws && !(SVW(o_wu + (k)) > RF)) --k;)
         const int kF = k;
-        PS_HOT_LOOP(while (k >= ws && !(SV(o_wu + (k)) > RG)) --k;)
+        PS_HOT_LOOP(while (k >= ws && !(SVW(o_wu + (k)) > RG)) --k;)
         auto conv = [&](V R, int kk) -> int {
             if (R < 0 || top > R) return TAU_NONE;
-            if (kk >= ws) return (int)SW(o_wt + (kk + 1));
-            return base > R && ws < we ? (int)SW(o_wt + (ws)) : TAU_ANY;
+            if (kk >= ws) return (int)SWW(o_wt + (kk + 1));
+            return base > R && ws < we ? (int)SWW(o_wt + (ws)) : TAU_ANY;
         };
         tauF = conv(RF, kF);
         tauG = conv(RG, k);
@@ -915,7 +923,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             const uint32_t *st = src + ck_t + i * p.ck_kc;
             const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
             PS_NOUNROLL_C for (int q = 0; q < we - ws && eq; ++q)
-                eq = (int)SW(o_wt + (ws + q)) - (int)st[q] == d && SV(o_wu + (ws + q)) == su[q];
+                eq = (int)SWW(o_wt + (ws + q)) - (int)st[q] == d && SVW(o_wu + (ws + q)) == su[q];
         }
         conv_delta = d;
 #ifdef PS_DEBUG_CONV
@@ -1161,7 +1169,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             if (has_stage) {
                 const uint32_t *st = src + ck_t + i * p.ck_kc;
                 const V *su = reinterpret_cast<const V *>(src + ck_u) + i * p.ck_kc;
-                PS_NOUNROLL_C for (int q = 0; q < we; ++q) { SW(o_wt + (q)) = st[q]; SV(o_wu + (q)) = su[q]; }
+                PS_NOUNROLL_C for (int q = 0; q < we; ++q) { SWW(o_wt + (q)) = st[q]; SVW(o_wu + (q)) = su[q]; }
                 wlo = we > 0 ? (int)st[0] : INT_MAX;
                 whi = we > 0 ? (int)st[we - 1] : INT_MIN;
             }
@@ -1290,7 +1298,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         if (has_stage) {
                             uint32_t *st = dst + ck_t + i * p.ck_kc;
                             V *su = reinterpret_cast<V *>(dst + ck_u) + i * p.ck_kc;
-                            PS_NOUNROLL_C for (int q = ws; q < we; ++q) { st[q - ws] = SW(o_wt + (q)); su[q - ws] = SV(o_wu + (q)); }
+                            PS_NOUNROLL_C for (int q = ws; q < we; ++q) { st[q - ws] = SWW(o_wt + (q)); su[q - ws] = SVW(o_wu + (q)); }
                         }
                         const int ws0 = ws, we0 = we;
                         we -= ws;
@@ -1583,6 +1591,8 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
 #undef SW
 #undef SV
 #undef SB
+#undef SWW
+#undef SVW
 }
 
 }  // namespace ps
