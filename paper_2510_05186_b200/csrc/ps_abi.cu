@@ -160,6 +160,19 @@ cudaError_t occupancy(bool v64, bool moves, Variant v, int block, size_t smem, i
     return moves ? eval_occupancy<int, true>(v, block, smem, n) : eval_occupancy<int, false>(v, block, smem, n);
 }
 
+int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+// Global-state kernels with nonzero-word masks over the pending-transfer sets: for stages with
+// many bitset words (config 5, MW = 8: 15.9 vs 17.5 ms per round); with few (config 4, MW = 4) the
+// plain scan is faster (4.29 vs 4.55 ms).
+bool wmask_shape(int MW) {
+    static const int on = env_int("PS_WMASK", 1);
+    return on && MW >= 6 && MW <= 16;
+}
+
 cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s,
                    bool record = false) {
     Variant v;
@@ -167,14 +180,11 @@ cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, Launc
     v.record = record;
     v.derived = p.chorders == nullptr;
     v.uni = p.uniform != 0;
+    v.wmask = gstate && wmask_shape(p.MW);
     if (v64) return moves ? eval_launch<long long, true>(v, p, c, s) : eval_launch<long long, false>(v, p, c, s);
     return moves ? eval_launch<int, true>(v, p, c, s) : eval_launch<int, false>(v, p, c, s);
 }
 
-int env_int(const char *name, int dflt) {
-    const char *v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 // Shared-memory plan for the main pass: one candidate per warp, ledger window K (12 by default, or
 // the whole 5m ledger when that is smaller and cannot overflow), as many warps per block as fit;
@@ -217,6 +227,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         v.record = false;
         v.derived = true;
         v.uni = I->uniform != 0;
+        v.wmask = pl->gstate && wmask_shape(I->MW);
         const uint64_t okey = ((uint64_t)pl->cfg.smem << 16) | ((uint64_t)pl->cfg.block << 2) |
                               ((uint64_t)pl->gstate << 1) | (uint64_t)moves;
         *per_sm = 0;

@@ -273,8 +273,11 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #endif
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
-template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 : GSTATE ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
+// GS: per-candidate state in shared memory (0), in global scratch (1), in global scratch with
+// nonzero-word masks over the pending-transfer sets (2: many bitset words per stage, config 5).
+template <typename V, bool MOVES, int GS, bool REC, bool DERIVED, bool UNI>
+__global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 : GS ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
+    constexpr bool GSTATE = GS != 0;
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
@@ -393,6 +396,10 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
     // zero below b_xlo, both zero from b_hi on (the slot starts unknown: everything is rewritten).
     // A recording tracks the same bounds to save them.
     constexpr bool BAND = GSTATE && !REC;
+    // Global state: which words of this stage's pending-offload (bits 0-15) and pending-reload
+    // (bits 16-31) sets are nonzero, so transfer_key skips the empty ones (config 5: 8 words each).
+    const bool wmask_on = GS == 2 && MW <= 16;     // (GS 2 is launched for 6 <= MW <= 16 only)
+    uint32_t pwm = 0;
     int b_alo = 0, b_xlo = 0, b_hi = m;
     // 16-byte vectors over the rows: row starts and checkpoints on 16-byte boundaries
     const bool band_vec = ((o_A | m | p.cand_words | p.ck_words) & 3) == 0;
@@ -584,22 +591,31 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
         const int C = cfree;
         const uint32_t stb = (uint32_t)i << 24;
         if (derived) {
-            if (n_poff)
-                for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = SB(o_poff + (w)); bits; bits &= bits - 1) {
-                        int j = w * 32 + __ffs(bits) - 1;
-                        best = min(best, make_key((uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C),
-                                                  (2u << 30) | stb | ((uint32_t)j << 2)));
-                    }
-            if (n_prel)
-                for (int w = 0; w < MW; ++w)
-                    for (uint32_t bits = SB(o_prel + (w)); bits; bits &= bits - 1) {
-                        int j = w * 32 + __ffs(bits) - 1;
-                        int tau = tau_G(limit_i - val_of(j, 3));
-                        if (tau == TAU_NONE) continue;
-                        best = min(best, make_key((uint32_t)max(max((int)(SW(o_Xi + (j)) >> 2), C), tau),
-                                                  (1u << 30) | stb | ((uint32_t)j << 2)));
-                    }
+            // (global state: only the words the nonzero-word masks name)
+            auto poff_word = [&](int w) {
+                for (uint32_t bits = SB(o_poff + (w)); bits; bits &= bits - 1) {
+                    int j = w * 32 + __ffs(bits) - 1;
+                    best = min(best, make_key((uint32_t)max((int)(SW(o_Ai + (j)) >> 2), C),
+                                              (2u << 30) | stb | ((uint32_t)j << 2)));
+                }
+            };
+            auto prel_word = [&](int w) {
+                for (uint32_t bits = SB(o_prel + (w)); bits; bits &= bits - 1) {
+                    int j = w * 32 + __ffs(bits) - 1;
+                    int tau = tau_G(limit_i - val_of(j, 3));
+                    if (tau == TAU_NONE) continue;
+                    best = min(best, make_key((uint32_t)max(max((int)(SW(o_Xi + (j)) >> 2), C), tau),
+                                              (1u << 30) | stb | ((uint32_t)j << 2)));
+                }
+            };
+            if (n_poff) {
+                if (wmask_on) for (uint32_t x = pwm & 0xFFFFu; x; x &= x - 1) poff_word(__ffs(x) - 1);
+                else for (int w = 0; w < MW; ++w) poff_word(w);
+            }
+            if (n_prel) {
+                if (wmask_on) for (uint32_t x = pwm >> 16; x; x &= x - 1) prel_word(__ffs(x) - 1);
+                else for (int w = 0; w < MW; ++w) prel_word(w);
+            }
         } else if (chead != NO_CHAN && (int)((chead >> 16) & 0x7FFFu) == i) {
             int j = chead & 0xFFFFu;
             if (!(chead >> 31)) {
@@ -1181,6 +1197,11 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                 for (int w = 0; w < MW; ++w) nb += __popc(SB(o_offm + (w)));
                 n_unrel += cand_unrel - nb;
                 build_mask(false);
+                if (wmask_on) {
+                    pwm = 0;
+                    for (int w = 0; w < MW; ++w)
+                        pwm |= (SB(o_poff + (w)) ? 1u << w : 0u) | (SB(o_prel + (w)) ? 1u << (16 + w) : 0u);
+                }
                 if (REC) {
                     // the kept checkpoints become the new base's: its offload bits, and the
                     // outstanding-transfer count that goes with them (the suffix-sharing compare
@@ -1206,6 +1227,7 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
             base = top = peak = 0; ws = we = 0;
             wlo = INT_MAX; whi = INT_MIN;
             n_poff = n_prel = 0;
+            pwm = 0;
             n_unrel = cand_unrel;
             first_start = INT_MAX; ecount = 0;
             cc = 0;
@@ -1355,7 +1377,11 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         // (every later write to row i, or row i's X, at microbatch j follows this F)
                         if (BAND || REC) b_hi = max(b_hi, j + 1);
                         SW(o_Ai + (j)) = ((uint32_t)end << 2) | 1u;
-                        if (newreq) { SB(o_poff + (j >> 5)) |= 1u << (j & 31); ++n_poff; }
+                        if (newreq) {
+                            SB(o_poff + (j >> 5)) |= 1u << (j & 31);
+                            ++n_poff;
+                            if (wmask_on) pwm |= 1u << (j >> 5);
+                        }
                         if (i > 0) {
                             // F(i, j) read A[i-1][j]; unless F(i-1, j)'s offload is still to come,
                             // only B(i-1, j) reads it now
@@ -1397,12 +1423,23 @@ __global__ void __launch_bounds__(GSTATE ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ?
                         SW(o_Xi + (j)) = 1u;
                         if (i == P - 1 || (SW(o_A + ((i + 1) * m + j)) & 3u) != 0u) SW(o_Ai + (j)) = 1u;
                         win_insert(end, -g);
-                        if (derived) { SB(o_poff + (j >> 5)) &= ~bit; SB(o_prel + (j >> 5)) |= bit; --n_poff; ++n_prel; }
+                        if (derived) {
+                            const uint32_t rest = SB(o_poff + (j >> 5)) & ~bit;
+                            SB(o_poff + (j >> 5)) = rest;
+                            SB(o_prel + (j >> 5)) |= bit;
+                            --n_poff; ++n_prel;
+                            if (wmask_on) pwm = (pwm & ~(rest ? 0u : 1u << (j >> 5))) | (1u << (16 + (j >> 5)));
+                        }
                     } else {
                         SW(o_Xi + (j)) = ((uint32_t)end << 2) | 2u;
                         win_insert(t, g);
                         --n_unrel;
-                        if (derived) { SB(o_prel + (j >> 5)) &= ~bit; --n_prel; }
+                        if (derived) {
+                            const uint32_t rest = SB(o_prel + (j >> 5)) & ~bit;
+                            SB(o_prel + (j >> 5)) = rest;
+                            --n_prel;
+                            if (wmask_on && !rest) pwm &= ~(1u << (16 + (j >> 5)));
+                        }
                     }
                     // the ledger changed: an F head re-fits; a B head may have been waiting on this reload
                     cdirty = cdirty || (pos < L && ((head & 3u) == KIND_F || head == (((uint32_t)j << 2) | KIND_B)));

@@ -22,13 +22,13 @@ static cudaError_t ensure_smem(Fn fn, size_t smem, std::atomic<int> *granted) {
 }
 
 // one grant record per kernel instantiation and device, shared by launches and occupancy queries
-template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
+template <typename V, bool MOVES, int GSTATE, bool REC, bool DERIVED, bool UNI>
 static std::atomic<int> *granted_for() {
     static std::atomic<int> g[64];
     return g;
 }
 
-template <typename V, bool MOVES, bool GSTATE, bool REC, bool DERIVED, bool UNI>
+template <typename V, bool MOVES, int GSTATE, bool REC, bool DERIVED, bool UNI>
 static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t stream) {
     auto fn = eval_kernel<V, MOVES, GSTATE, REC, DERIVED, UNI>;
     cudaError_t e = ensure_smem(fn, cfg.smem, granted_for<V, MOVES, GSTATE, REC, DERIVED, UNI>());
@@ -37,7 +37,7 @@ static cudaError_t launch_one(const EvalParams &p, LaunchCfg cfg, cudaStream_t s
     return cudaGetLastError();
 }
 
-template <typename V, bool MOVES, bool GSTATE, bool DERIVED, bool UNI>
+template <typename V, bool MOVES, int GSTATE, bool DERIVED, bool UNI>
 static cudaError_t occ_one(int block, size_t smem, int *n) {
     auto fn = eval_kernel<V, MOVES, GSTATE, false, DERIVED, UNI>;
     cudaError_t e = ensure_smem(fn, smem, granted_for<V, MOVES, GSTATE, false, DERIVED, UNI>());
@@ -49,21 +49,23 @@ static cudaError_t occ_one(int block, size_t smem, int *n) {
 // single materialised candidate in derived mode with its state in shared memory.
 #define PS_PICK(FN, ARGS)                                                                              \
     if (!MOVES && v.record)                                                                           \
-        return v.uni ? FN<V, false, false, true, true, true> ARGS : FN<V, false, false, true, true, false> ARGS; \
+        return v.uni ? FN<V, false, 0, true, true, true> ARGS : FN<V, false, 0, true, true, false> ARGS; \
     if (MOVES || v.derived) {                                                                         \
-        if (v.gstate) return v.uni ? FN<V, MOVES, true, false, true, true> ARGS : FN<V, MOVES, true, false, true, false> ARGS; \
-        return v.uni ? FN<V, MOVES, false, false, true, true> ARGS : FN<V, MOVES, false, false, true, false> ARGS; \
+        if (v.gstate && v.wmask) return v.uni ? FN<V, MOVES, 2, false, true, true> ARGS : FN<V, MOVES, 2, false, true, false> ARGS; \
+        if (v.gstate) return v.uni ? FN<V, MOVES, 1, false, true, true> ARGS : FN<V, MOVES, 1, false, true, false> ARGS; \
+        return v.uni ? FN<V, MOVES, 0, false, true, true> ARGS : FN<V, MOVES, 0, false, true, false> ARGS; \
     }                                                                                                 \
-    if (v.gstate) return v.uni ? FN<V, false, true, false, false, true> ARGS : FN<V, false, true, false, false, false> ARGS; \
-    return v.uni ? FN<V, false, false, false, false, true> ARGS : FN<V, false, false, false, false, false> ARGS;
+    if (v.gstate) return v.uni ? FN<V, false, 1, false, false, true> ARGS : FN<V, false, 1, false, false, false> ARGS; \
+    return v.uni ? FN<V, false, 0, false, false, true> ARGS : FN<V, false, 0, false, false, false> ARGS;
 
 #define PS_PICK_OCC(FN, ARGS)                                                                          \
     if (MOVES || v.derived) {                                                                         \
-        if (v.gstate) return v.uni ? FN<V, MOVES, true, true, true> ARGS : FN<V, MOVES, true, true, false> ARGS; \
-        return v.uni ? FN<V, MOVES, false, true, true> ARGS : FN<V, MOVES, false, true, false> ARGS; \
+        if (v.gstate && v.wmask) return v.uni ? FN<V, MOVES, 2, true, true> ARGS : FN<V, MOVES, 2, true, false> ARGS; \
+        if (v.gstate) return v.uni ? FN<V, MOVES, 1, true, true> ARGS : FN<V, MOVES, 1, true, false> ARGS; \
+        return v.uni ? FN<V, MOVES, 0, true, true> ARGS : FN<V, MOVES, 0, true, false> ARGS; \
     }                                                                                                 \
-    if (v.gstate) return v.uni ? FN<V, false, true, false, true> ARGS : FN<V, false, true, false, false> ARGS; \
-    return v.uni ? FN<V, false, false, false, true> ARGS : FN<V, false, false, false, false> ARGS;
+    if (v.gstate) return v.uni ? FN<V, false, 1, false, true> ARGS : FN<V, false, 1, false, false> ARGS; \
+    return v.uni ? FN<V, false, 0, false, true> ARGS : FN<V, false, 0, false, false> ARGS;
 
 template <typename V, bool MOVES>
 cudaError_t eval_launch(Variant v, const EvalParams &p, LaunchCfg cfg, cudaStream_t s) {

@@ -15,6 +15,7 @@ struct Variant {
     bool record;    // base recording (checkpoints)
     bool derived;   // greedy channel mode
     bool uni;       // microbatch-symmetric instance tables
+    bool wmask;     // (global state) nonzero-word masks over the pending-transfer sets
 };
 
 // One translation unit per (ledger value type V, move-encoded candidates).
