@@ -268,6 +268,9 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #ifndef PS_MIN_BLOCKS_MAT
 #define PS_MIN_BLOCKS_MAT 5   // materialised candidates: 102-register cap (r01 A/B)
 #endif
+#ifndef PS_REC_BAND_CMP
+#define PS_REC_BAND_CMP 1     // recordings compare row bands (per lane) rather than whole rows (warp-wide)
+#endif
 #ifndef PS_TAU_PAIR
 #define PS_TAU_PAIR 0   // measured slower on B200 (r01): register pressure outweighs the saved scan
 #endif
@@ -728,15 +731,48 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
     // Recording: drop every such time at each checkpoint boundary, so checkpoints hold only times
     // that still matter (simulations are unchanged; state bits are untouched, so the predicates
     // other lanes read meanwhile are stable).
+    // dom_bound for a word of this lane's own rows (j: microbatch, st: its state), given the
+    // neighbouring stages' free times: no shuffles, for per-lane loops over the row bands.
+    auto own_bound = [&](bool isA, int j, uint32_t st, int sf_up, int sf_dn) -> int {
+        int bound = INT_MAX;
+        if (isA && st == 1u) {
+            if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
+            if (((SB(o_offm + (j >> 5)) >> (j & 31)) & 1u) && (SW(o_Xi + (j)) & 3u) == 0u) bound = min(bound, cfree);
+        } else if (isA) {
+            if (i > 0 && (SW(o_A + ((i - 1) * m + j)) & 3u) < 2u) bound = min(bound, sf_dn - p.comm);
+        } else if (st == 2u) {
+            bound = min(bound, sfree);
+        }
+        return bound;
+    };
     auto canon_dominated = [&]() {
-        const int n2 = 2 * P * m;
-        for (int k0 = 0; k0 < n2; k0 += 32) {
-            const int k = k0 + lane;
-            const uint32_t w = k < n2 ? SW(o_A + (k)) : 0u;
-            const bool timed = (w >> 2) != 0u && w != A_DEAD;
-            if (!__any_sync(0xffffffffu, timed)) continue;
-            const int bound = dom_bound(timed, k, w);
-            if (timed && bound != INT_MAX && (int)(w >> 2) <= bound) SW(o_A + (k)) = w & 3u;
+        // each lane over its own rows' band (outside it no word carries a time)
+        const int sf_up = __shfl_sync(0xffffffffu, sfree, min(i + 1, 31));
+        const int sf_dn = __shfl_sync(0xffffffffu, sfree, max(i - 1, 0));
+        if (has_stage) {
+            while (b_alo < b_hi && SW(o_Ai + (b_alo)) == A_DEAD) ++b_alo;
+            auto canon = [&](bool isA, int j, uint32_t w) -> uint32_t {
+                if ((w >> 2) == 0u || w == A_DEAD) return w;
+                const int bound = own_bound(isA, j, w & 3u, sf_up, sf_dn);
+                return bound != INT_MAX && (int)(w >> 2) <= bound ? (w & 3u) : w;
+            };
+            for (int r = 0; r < 2; ++r) {
+                const int off = r == 0 ? o_Ai : o_Xi;
+                if (band_vec) {
+                    // four words per 16-byte access (the widened words are A_DEAD or zero: unchanged)
+                    uint4 *row4 = reinterpret_cast<uint4 *>(&SW(off));
+#pragma unroll 1
+                    for (int k = b_alo >> 2; k < (b_hi + 3) >> 2; ++k) {
+                        const uint4 v = row4[k];
+                        const uint4 c = make_uint4(canon(r == 0, 4 * k, v.x), canon(r == 0, 4 * k + 1, v.y),
+                                                   canon(r == 0, 4 * k + 2, v.z), canon(r == 0, 4 * k + 3, v.w));
+                        if (c.x != v.x || c.y != v.y || c.z != v.z || c.w != v.w) row4[k] = c;
+                    }
+                } else {
+#pragma unroll 1
+                    for (int j = b_alo; j < b_hi; ++j) SW(off + (j)) = canon(r == 0, j, SW(off + (j)));
+                }
+            }
         }
         __syncwarp();
     };
@@ -801,7 +837,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         // be irrelevant in the candidate too (dom_bound); state-only words must be equal
         const uint32_t d4 = (uint32_t)d << 2;
         const int n2 = 2 * P * m;
-        if constexpr (BAND) {
+        if constexpr (BAND || (REC && PS_REC_BAND_CMP)) {
             // Each lane compares its own stage's rows over the union of the two bands (outside it
             // both sides are A_DEAD below and zero above), 16-byte vectors, two of each in flight.
             // dom_bound's readers are this stage's neighbours: their free times are shuffled once.
@@ -815,17 +851,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
                     const bool timed_c = (cw >> 2) != 0u && cw != A_DEAD, timed_b = (bw >> 2) != 0u && bw != A_DEAD;
                     if (timed_c == timed_b && (timed_c ? cw - bw == d4 : cw == bw)) return true;
                     if (!(timed_c && !timed_b && (cw & 3u) == bw)) return false;
-                    int bound = INT_MAX;                  // dom_bound for a word of this lane's rows
-                    const uint32_t st = cw & 3u;
-                    if (isA && st == 1u) {
-                        if (i + 1 < P && (SW(o_A + ((i + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
-                        if (((SB(o_offm + (j >> 5)) >> (j & 31)) & 1u) && (SW(o_Xi + (j)) & 3u) == 0u)
-                            bound = min(bound, cfree);
-                    } else if (isA) {
-                        if (i > 0 && (SW(o_A + ((i - 1) * m + j)) & 3u) < 2u) bound = min(bound, sf_dn - p.comm);
-                    } else if (st == 2u) {
-                        bound = min(bound, sfree);
-                    }
+                    const int bound = own_bound(isA, j, cw & 3u, sf_up, sf_dn);
                     return bound != INT_MAX && (int)(cw >> 2) <= bound;
                 };
                 auto cmp_row = [&](bool isA, int row_off, const uint32_t *brow, int lo) -> bool {
