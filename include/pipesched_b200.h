@@ -51,7 +51,9 @@ extern "C" {
 #define PS_FLAG_FEASIBLE 1u     /* complete schedule; STRICT peak <= limit by construction */
 #define PS_FLAG_DEADLOCK 2u     /* no event can start: the reference raises OrderInfeasible */
 #define PS_FLAG_MALFORMED 4u    /* an op code names no op of its stage / bad offload bit / bad channel order */
-#define PS_FLAG_RANGE 16u       /* an event time of this candidate reached 2^29 quanta (not evaluated)   */
+#define PS_FLAG_RANGE 16u       /* an event time reached 2^29 quanta: search rounds drop the neighbour;
+                                   ps_eval_batch finishes it in 64-bit time and keeps the flag only
+                                   when a trace was requested and a time passes 2^31 - 1            */
 
 /* Stage rows: 3m op codes (microbatch << 2 | kind), or fewer ending with PS_ROW_END (0xFFFF;
    0xFF for uint8 codes).  A row that repeats an op or is short is replayed literally, as the

@@ -682,8 +682,9 @@ int ps_instance_create(const ps_instance_desc *d, int device, ps_instance **out)
     // Event times are packed as (t << 2 | state) in 32 bits, so every event must end below 2^29.
     // Durations must fit well inside that; the instance's horizon (no event of any structure can
     // end later) decides whether the kernels check at all: past it, an event chosen to start at or
-    // after 2^29 - (longest duration) ends that candidate with PS_FLAG_RANGE (ps_eval.cuh), so
-    // instances with long horizons are accepted and every schedule whose times fit is exact.
+    // after 2^29 - (longest duration) ends that candidate with PS_FLAG_RANGE (ps_eval.cuh), and
+    // ps_eval_batch finishes it in 64-bit time (ps_literal.cu): instances with long horizons are
+    // accepted and every candidate is exact.  (Search rounds do not adopt such a neighbour.)
     int64_t max_dur = std::max<int64_t>(d->comm_time, d->offload_time);
     for (size_t k = 0; k < (size_t)P * m * 3; ++k) max_dur = std::max<int64_t>(max_dur, d->proc_time[k]);
     if (max_dur >= (int64_t)1 << 27)
@@ -1272,7 +1273,8 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     p.makespan = makespan_out;
     p.best_key = (long long *)best_key;
     p.dedup = makespan_out == nullptr && d->dedup;
-    p.cutoff = makespan_out == nullptr && d->cutoff > 0 ? d->cutoff : 0;
+    // (bound pruning sums a stage's remaining work in 32 bits: only where the horizon fits them)
+    p.cutoff = makespan_out == nullptr && d->cutoff > 0 && I->time_safe == INT_MAX ? d->cutoff : 0;
     p.events_total = (unsigned long long *)d->events_total;
     return run_eval(I, p, true, (cudaStream_t)stream, d->base);
 }

@@ -14,8 +14,14 @@
 // stage (microbatch >= m, kind 3) or whose offload bits name a non-offloadable F stays MALFORMED
 // (the reference raises KeyError or worse there).
 //
-// Rare by construction (malformed input), so the simplest correct mapping: one thread per
-// candidate, state in a global scratch slot, a few thousand slots at most.
+// The same pass finishes, in 64-bit time, every candidate the evaluator ended with PS_FLAG_RANGE
+// (an event time reached 2^29 quanta, the limit of its packed 32-bit end-time words): makespan,
+// bubble, STRICT peaks and the commit-ordered trace as the reference computes them
+// (schedule.py:168-237, cli.py:115), so instances with long horizons get exact answers for every
+// candidate (a trace time that does not fit the int32 trace output keeps PS_FLAG_RANGE).
+//
+// Rare by construction (malformed input, very long schedules), so the simplest correct mapping:
+// one thread per candidate, state in a global scratch slot, a few thousand slots at most.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <climits>
@@ -87,17 +93,26 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
     int64_t *rel_end = off_end + (size_t)P * m;    // [P*m]
     int64_t *sfree = rel_end + (size_t)P * m;      // [P]
     int64_t *cfree = sfree + P;                    // [G]
+    int64_t *first_start = cfree + G;              // [P] start of the stage's first compute
+    // earliest_fit answers, cached until the stage's ledger grows (its point count is its version):
+    // the F head's per stage (keyed by position and floor), each reload's per activation (by floor)
+    int64_t *fc_lo = first_start + P, *fc_res = fc_lo + P;              // [P]
+    int64_t *rc_lo = fc_res + P, *rc_res = rc_lo + (size_t)P * m;       // [P*m]
     const int cap = 5 * m + 8;                     // ledger points per stage: <= len(row) + 2m
-    Pt *pts = reinterpret_cast<Pt *>(cfree + G);   // [P][cap]
+    Pt *pts = reinterpret_cast<Pt *>(rc_res + (size_t)P * m);   // [P][cap]
     int32_t *ints = reinterpret_cast<int32_t *>(pts + (size_t)P * cap);
     int32_t *npts = ints;                          // [P]
     int32_t *pos = npts + P;                       // [P]
     int32_t *len = pos + P;                        // [P]
     int32_t *cpos = len + P;                       // [G]
-    uint8_t *req = reinterpret_cast<uint8_t *>(cpos + G);   // [P*m] bit0 offload, bit1 reload requested
+    int32_t *fc_n = cpos + G, *fc_pos = fc_n + P;  // [P] cache keys: ledger points, head position
+    int32_t *rc_n = fc_pos + P;                    // [P*m]
+    int32_t *pend = rc_n + (size_t)P * m;          // [P*m] (derived mode) requested, not yet reloaded
+    uint8_t *req = reinterpret_cast<uint8_t *>(pend + (size_t)P * m);   // [P*m] bit0 offload, bit1 reload requested
     const int mwords = (P * m + 31) / 32;
     for (int64_t c = tid; c < p.N; c += slots) {
-        if (p.flags[c] != FLAG_MALFORMED) continue;
+        const uint32_t flag_in = p.flags[c];
+        if (flag_in != FLAG_MALFORMED && flag_in != FLAG_RANGE) continue;
         // ---- op codes and offload bits must name ops of the instance --------------------------
         bool bad = false;
         auto code_at = [&](int i, int q) -> uint32_t {
@@ -138,16 +153,22 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
         // ---- run_order, literally (listsched.py:170-267) ------------------------------------
         for (int k = 0; k < P * m * 3; ++k) done[k] = -1;
         for (int k = 0; k < P * m; ++k) { off_end[k] = rel_end[k] = -1; req[k] = 0; }
-        for (int i = 0; i < P; ++i) { sfree[i] = 0; npts[i] = 0; pos[i] = 0; }
+        for (int i = 0; i < P; ++i) { sfree[i] = 0; npts[i] = 0; pos[i] = 0; fc_n[i] = -1; }
+        for (int k = 0; k < P * m; ++k) rc_n[k] = -1;
         for (int g = 0; g < G; ++g) { cfree[g] = 0; cpos[g] = 0; }
         const bool derived = p.chorders == nullptr;
         const long long total = 3LL * P * m, total_tr = 2LL * n_off;
         long long n_done = 0, n_tr = 0;
+        int n_pend = 0;
         auto proc = [&](int i, int j, int k) -> int64_t { return p.proc[((p.uniform ? i : i * m + j)) * 3 + k]; };
         auto vrow = [&](int i, int j, int k) -> int64_t { return val<V>(p.vals, (p.uniform ? i : i * m + j) * 4 + k); };
         auto D = [&](int i, int j, int k) -> int64_t & { return done[((size_t)i * m + j) * 3 + k]; };
         uint32_t blocked = 0u;
         bool deadlock = false;
+        long long ecount = 0;
+        bool trace_ovf = false;
+        int64_t lo_start = INT64_MAX, hi_end = INT64_MIN;
+        for (int i = 0; i < P; ++i) first_start[i] = INT64_MAX;
         while (n_done < total || n_tr < total_tr) {
             // (the derived-mode pending list is the requested set minus what was committed:
             // selection below is by the minimum key, so the list order never matters)
@@ -182,7 +203,13 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
                 if (!ready) continue;
                 int64_t lo = max(fl, sfree[i]);
                 if (k == KIND_F) {
-                    lo = earliest_fit(pts + (size_t)i * cap, npts[i], val<V>(p.limit, i), lo, vrow(i, j, 0), proc(i, j, 0));
+                    if (fc_n[i] != npts[i] || fc_pos[i] != pos[i] || fc_lo[i] != lo) {
+                        fc_n[i] = npts[i];
+                        fc_pos[i] = pos[i];
+                        fc_lo[i] = lo;
+                        fc_res[i] = earliest_fit(pts + (size_t)i * cap, npts[i], val<V>(p.limit, i), lo, vrow(i, j, 0), proc(i, j, 0));
+                    }
+                    lo = fc_res[i];
                     if (lo == T_NONE) continue;
                 }
                 if (better(lo, RANK_COMPUTE, i, j, k)) { bt = lo; brank = RANK_COMPUTE; bi = i; bj = j; bk = k; }
@@ -193,18 +220,23 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
                 int64_t lo = max(floor_t, cfree[g]);
                 const int i = x / m, j = x % m;
                 if (reload) {
-                    lo = earliest_fit(pts + (size_t)i * cap, npts[i], val<V>(p.limit, i), lo, vrow(i, j, 3), 0);
+                    if (rc_n[x] != npts[i] || rc_lo[x] != lo) {
+                        rc_n[x] = npts[i];
+                        rc_lo[x] = lo;
+                        rc_res[x] = earliest_fit(pts + (size_t)i * cap, npts[i], val<V>(p.limit, i), lo, vrow(i, j, 3), 0);
+                    }
+                    lo = rc_res[x];
                     if (lo == T_NONE) return;
                 }
                 const int rank = reload ? RANK_RELOAD : RANK_OFFLOAD;
                 if (better(lo, rank, i, j, 0)) { bt = lo; brank = rank; bi = i; bj = j; bk = 0; bg = g; }
             };
             if (derived) {
-                for (int x = 0; x < P * m; ++x) {
-                    if (!offloaded(x)) continue;
-                    // refresh (listsched.py:207-214): requests appear once their producer commits
-                    if (D(x / m, x % m, 0) >= 0) req[x] |= 1;
-                    if (off_end[x] >= 0) req[x] |= 2;
+                // refresh (listsched.py:207-214): a request appears once its producer commits (the
+                // commits below keep the requested-not-reloaded activations in `pend`; selection is
+                // by the minimum key, so the list order never matters)
+                for (int q = 0; q < n_pend; ++q) {
+                    const int x = pend[q];
                     const int g = p.chan[x / m];
                     if ((req[x] & 1) && !(req[x] & 4)) transfer(g, x, false);      // bit 2: offload committed
                     if ((req[x] & 2) && !(req[x] & 8)) transfer(g, x, true);       // bit 3: reload committed
@@ -223,10 +255,26 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
                 deadlock = true;
                 break;
             }
+            if (p.tcode) {                                          // commit-ordered trace
+                if (bt > INT_MAX) trace_ovf = true;
+                else if (ecount < p.tstride) {
+                    p.tcode[(size_t)c * p.tstride + ecount] = ((uint32_t)brank << 30) | ((uint32_t)bi << 24) |
+                                                              ((uint32_t)bj << 2) | (uint32_t)bk;
+                    p.tstart[(size_t)c * p.tstride + ecount] = (int32_t)bt;
+                }
+            }
+            ++ecount;
             if (brank == RANK_COMPUTE) {                            // _commit_compute (148-152)
                 const int64_t end = bt + proc(bi, bj, bk);
+                lo_start = min(lo_start, bt);
+                hi_end = max(hi_end, end);
+                if (first_start[bi] == INT64_MAX) first_start[bi] = bt;
                 if (D(bi, bj, bk) < 0) ++n_done;                    // len(done) counts distinct ops
                 D(bi, bj, bk) = end;
+                if (derived && bk == KIND_F && offloaded(bi * m + bj) && !(req[bi * m + bj] & 1)) {
+                    req[bi * m + bj] |= 1;                          // offload requested
+                    pend[n_pend++] = bi * m + bj;
+                }
                 ledger_add(pts + (size_t)bi * cap, &npts[bi], end, vrow(bi, bj, bk));
                 ++pos[bi];
                 sfree[bi] = end;
@@ -236,20 +284,55 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
                 if (brank == RANK_OFFLOAD) {
                     off_end[x] = end;
                     ledger_add(pts + (size_t)bi * cap, &npts[bi], end, -gamma);
-                    req[x] |= 4;
+                    req[x] |= 4 | 2;                                // committed; reload requested
                 } else {
                     rel_end[x] = end;
                     ledger_add(pts + (size_t)bi * cap, &npts[bi], bt, gamma);
                     req[x] |= 8;
+                    if (derived)
+                        for (int q = 0; q < n_pend; ++q)
+                            if (pend[q] == x) { pend[q] = pend[--n_pend]; break; }
                 }
                 cfree[bg] = end;
                 if (!derived) ++cpos[bg];
                 ++n_tr;
             }
         }
-        if (!deadlock) continue;   // unreachable for rows that miss an op; left MALFORMED if it were
+        if (p.events_total) atomicAdd(p.events_total, (unsigned long long)ecount);
+        if (!deadlock) {
+            // (rows that miss an op cannot get here; a range candidate finishes)
+            if (flag_in != FLAG_RANGE || trace_ovf) continue;
+            // makespan (schedule.py:168-183): global compute span, or the worst per-stage span
+            int64_t span;
+            if (p.post) {
+                span = 0;
+                for (int i = 0; i < P; ++i) span = max(span, sfree[i] - first_start[i]);
+            } else {
+                span = hi_end - lo_start;
+            }
+            if (p.events_total) atomicAdd(p.events_total + 1, (unsigned long long)(total + total_tr));
+            p.flags[c] = FLAG_FEASIBLE;
+            if (p.makespan) p.makespan[c] = span;
+            if (p.bubble)
+                p.bubble[c] = span > 0 ? 1.0 - (double)p.busy / ((double)P * (double)span)
+                                       : __longlong_as_double(0x7ff8000000000000LL);
+            if (p.blocked) p.blocked[c] = 0u;
+            if (p.peak)
+                for (int i = 0; i < P; ++i) {
+                    // STRICT memory_trace peak (schedule.py:207-237): prefix sums of same-time merged deltas
+                    const Pt *q = pts + (size_t)i * cap;
+                    int64_t run = 0, pk = 0;
+                    for (int k = 0; k < npts[i];) {
+                        const int64_t t0 = q[k].t;
+                        while (k < npts[i] && q[k].t == t0) run += q[k++].d;
+                        pk = max(pk, run);
+                    }
+                    p.peak[(size_t)c * P + i] = pk * p.unit;
+                }
+            continue;
+        }
         p.flags[c] = FLAG_DEADLOCK;
-        p.makespan[c] = -1;
+        if (p.makespan) p.makespan[c] = -1;
         if (p.bubble) p.bubble[c] = __longlong_as_double(0x7ff8000000000000LL);
         if (p.blocked) p.blocked[c] = blocked;
         if (p.peak)
@@ -260,9 +343,9 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
 }  // namespace
 
 size_t literal_slot_bytes(int P, int m, int G) {
-    const size_t words = (size_t)P * m * 3 + 2 * (size_t)P * m + P + G;
+    const size_t words = (size_t)P * m * 3 + 4 * (size_t)P * m + 4 * P + G;
     const size_t pts = (size_t)P * (5 * m + 8) * sizeof(Pt);
-    const size_t ints = (size_t)(3 * P + G) * 4 + (size_t)P * m;
+    const size_t ints = (size_t)(5 * P + G) * 4 + 2 * (size_t)P * m * 4 + (size_t)P * m;
     return (words * 8 + pts + ints + 15) & ~(size_t)15;
 }
 

@@ -123,8 +123,8 @@ def run_orders(inst, candidates, explicit=False, device=None, types=None):
             stages = [i + 1 for i in range(pk.num_stages) if (m >> i) & 1]
             out.append(OrderInfeasible(f"no event can start (stages blocked: {stages})", stages))
         elif f & N.FLAG_RANGE:
-            raise ValueError(f"candidate {c}: an event time reaches 2^29 quanta, beyond the kernels' time "
-                             "range (DESIGN.md §7)")
+            raise ValueError(f"candidate {c}: an event time passes 2^31 - 1 quanta, beyond the int32 trace "
+                             "output (DESIGN.md §7)")
         else:
             raise ValueError(f"candidate {c} is malformed (flags {f:#x})")
     return out
