@@ -321,13 +321,14 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
     // relative to their start: after the rows in the state block, or (global-state passes) in the
     // warp's slice of shared memory behind the incumbent, where the event loop's many reads of them
     // stay on chip (checkpoints keep them after the rows either way).
-    const int o_offm = is * MW;                                 // [P][MW] offloaded bits
+    const int o_bits = GSTATE ? 0 : o_A + 2 * P * m;           // bitsets' start, in SB() offsets
+    const int o_offm = o_bits + is * MW;                        // [P][MW] offloaded bits
     const int o_poff = o_offm + P * MW;                         // [P][MW] pending offload requests
     const int o_prel = o_poff + P * MW;                         // [P][MW] pending reload requests
     const int nb3 = 3 * P * MW;                                 // bitset words
     const int nz = 2 * P * m + nb3;                      // words zeroed per candidate
     const int sbits = p.inc_words + warp * ((nb3 + 3) & ~3);    // (global state) shared-memory bitsets
-#define SB(off) (GSTATE ? smem[sbits + (off)] : smem[sbase + o_A + 2 * P * m + (off)])
+#define SB(off) (GSTATE ? smem[sbits + (off)] : smem[sbase + (off)])
     // Ledger windows (offsets o_wu / o_wt from the state start): with win_smem, a global-state pass
     // keeps them in the warp's shared-memory slice behind all warps' bitsets (same layout).
     uint32_t *const wsw = !GSTATE ? nullptr
@@ -717,7 +718,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
             const uint32_t st = w & 3u;
             if (isA && st == 1u) {          // F end: F(si+1, j), and F(si, j)'s offload
                 if (si + 1 < P && (SW(o_A + ((si + 1) * m + j)) & 3u) == 0u) bound = min(bound, sf_up - p.comm);
-                if (((SB(si * MW + (j >> 5)) >> (j & 31)) & 1u) &&
+                if (((SB(o_bits + si * MW + (j >> 5)) >> (j & 31)) & 1u) &&
                     (SW(o_A + (P * m + si * m + j)) & 3u) == 0u)
                     bound = min(bound, cf_own);
             } else if (isA) {               // B end: B(si-1, j)
@@ -957,7 +958,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         if (!__all_sync(0xffffffffu, eq)) { dbg(7); return false; }
 #endif
         PS_NOUNROLL_C for (int k = P * MW + lane; k < nb3; k += 32)     // (offm skipped: its differences are dead)
-            eq = eq && SB(k) == src[2 * P * m + k];
+            eq = eq && SB(o_bits + k) == src[2 * P * m + k];
 #ifdef PS_DEBUG_CONV
         if (!__all_sync(0xffffffffu, eq)) { dbg(8); return false; }
 #endif
@@ -1001,7 +1002,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         }
         // ================= initialise ======================================================
         // (BAND: the rows are rewritten over their bands by the restore below; only the bitsets here)
-        if (BAND) warp_zero_words_any(&SB(0), nb3, lane);
+        if (BAND) warp_zero_words_any(&SB(o_bits), nb3, lane);
         else warp_zero_words(&SW(o_A), nz, lane);
         if (!MOVES) {
             // stage the candidate's rows: 8-byte loads, coalesced across the warp
@@ -1189,7 +1190,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
             }
             if (BAND) {
                 // the bitsets, then each stage's rows over the old and the checkpoint's band
-                warp_copy_words_any(&SB(0), src + 2 * P * m, nb3, lane);
+                warp_copy_words_any(&SB(o_bits), src + 2 * P * m, nb3, lane);
                 if (has_stage) {
                     const uint32_t *rgs = src + ck_r + lane * CK_REGW;
                     const int clo = (int)rgs[21], chi = (int)rgs[22];
@@ -1411,7 +1412,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
                         if (i > 0) {
                             // F(i, j) read A[i-1][j]; unless F(i-1, j)'s offload is still to come,
                             // only B(i-1, j) reads it now
-                            const bool off_pending = ((SB((i - 1) * MW + (j >> 5)) >> (j & 31)) & 1u) &&
+                            const bool off_pending = ((SB(o_bits + (i - 1) * MW + (j >> 5)) >> (j & 31)) & 1u) &&
                                                      (SW(o_A + (P * m + (i - 1) * m + j)) & 3u) == 0u;
                             if (!off_pending) SW(o_A + ((i - 1) * m + j)) = 1u;
                         }
