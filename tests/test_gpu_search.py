@@ -518,3 +518,41 @@ def test_bound_pruning_keeps_every_round_decision(cuda_ok, late):
             ls.round = rnd
             ls.finish_round()
     assert adopted >= 1 or late
+
+
+@pytest.mark.parametrize("late", [False, True])
+def test_suffix_sharing_equals_full_simulation(cuda_ok, late):
+    """Every neighbour of config-3 search rounds (65,536 each, from the warm start and from the late
+    incumbent, where the convergence rules for finished stages and idle links matter most): its
+    makespan with prefix/suffix sharing against the recorded incumbent equals its full simulation,
+    and so does the peak of every stage on a materialised sample."""
+    import ctypes as C
+    import torch
+    from paper_2510_05186_b200 import _native as N
+    inst, orders, off, LocalSearch, SearchConfig = _setup(3)
+    n = 65536
+    ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n, shift_permille=PERMILLE,
+                                                     max_shift=MAXSHIFT))
+    if late:
+        z = np.load(Path(__file__).parent / "golden" / "inc320_config3.npz")
+        ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
+        ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
+        ls.base.record(ls.inc_orders, ls.inc_mask)
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for rnd in (0, 1):
+        got = []
+        for base in (ls.base, None):
+            out = torch.empty(n, dtype=torch.int64, device="cuda")
+            ls.best_key.fill_(N.BEST_NONE)
+            desc = N.SearchDesc(ls.inc_orders.data_ptr(), ls.inc_mask.data_ptr(), rnd, 0, n, ls.moves, None,
+                                base.handle if base is not None else None)
+            N.check(ls.lib.ps_search_round(ls.di.handle, C.byref(desc), C.c_void_p(ls.best_key.data_ptr()),
+                                           C.c_void_p(out.data_ptr()), stream))
+            torch.cuda.synchronize()
+            got.append((out.cpu().numpy(), int(ls.best_key.item())))
+        (a, ka), (b, kb) = got
+        assert (a == b).all(), (rnd, int((a != b).sum()))
+        assert ka == kb
+    # peaks and bubbles: materialised neighbours with and without the base
+    o, mk = ls.materialize(0, 4096, 0)
+    _eval_both(ls.di, o, mk, ls.base)
