@@ -510,8 +510,10 @@ def main():
         line["e2e"] = {"value": n_cand * world * K / d_s, "unit": UNIT, "h2d_bytes_per_step": h2d_d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": 1000 * d_s / K,
                        "api": "ps_eval_batch_host_delta: pinned host buffers holding the neighbours as differences "
-                              "from the incumbent (ps_delta_batch), copied in, rebuilt and evaluated on the device "
-                              "with the incumbent as the recorded base, results copied out, every step",
+                              "from the incumbent (ps_delta_batch), copied in, classified on the device (a candidate "
+                              "that is one move of the incumbent runs on the move-encoded kernel against its "
+                              "recorded base, any other is rebuilt and evaluated materialised), results copied out, "
+                              "every step",
                        "outputs": "makespan, bubble, per-stage STRICT peak, flags per candidate",
                        "outputs_equal_to_e2e_rows": same_d}
         # the same batch as a generic one: no recorded base, every candidate simulated from its

@@ -215,8 +215,12 @@ int ps_eval_batch_host(const ps_instance *inst, const ps_cand_batch *batch,
                        const ps_result_batch *results, void *stream);
 
 /* ps_eval_batch_host on a delta-encoded batch (HOST buffers, results to HOST, synchronous): the
-   differences cross PCIe, the full candidates are rebuilt in HBM by a kernel and evaluated in
-   derived channel mode. */
+   differences cross PCIe and are classified on the device.  A candidate that is one move of the
+   reference structure (one stage's contiguous run holding the reference run rotated by one, one
+   offloadable bit flipped, or nothing) is evaluated by the move-encoded kernel against the
+   reference (with prefix/suffix sharing when `base` was recorded on the reference); any other is
+   rebuilt in HBM and evaluated materialised.  Derived channel mode.  Out-of-range entries or
+   offsets fail the call (PS_ERR_INVALID) after the batch has run. */
 int ps_eval_batch_host_delta(const ps_instance *inst, const ps_delta_batch *batch,
                              const ps_result_batch *results, void *stream);
 

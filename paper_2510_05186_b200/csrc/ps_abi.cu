@@ -321,7 +321,9 @@ void refresh_info(const ps_base *B) {
     B->info_pending = false;
 }
 
-int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr) {
+// first_list (optional, device [count][indices]): the candidates the first pass evaluates.
+int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, const ps_base *B = nullptr,
+             const int32_t *first_list = nullptr) {
     if (p.N <= 0) return PS_OK;
     if (p.N > INT32_MAX) return fail(PS_ERR_RANGE, "at most 2^31-1 candidates per call");
     const int full = 5 * I->m;
@@ -360,7 +362,7 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
         q.cand_words = pl.cand_words;
         q.inc_words = pl.inc_words;
         q.win_smem = pl.gstate && pl.win_smem;
-        int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order;         // handoff k-1
+        const int32_t *in = k > 0 ? lists + (size_t)(k - 1) * list_words : order ? order : first_list;   // handoff k-1
         int32_t *out = k + 1 < npass ? lists + (size_t)k * list_words : nullptr;      // handoff k
         q.work_count = in;
         q.work_list = in ? in + 1 : nullptr;
@@ -502,11 +504,11 @@ MoveCtx move_ctx(const ps_instance *I);
 
 __global__ void divergence_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first, int64_t count,
                                   const uint32_t *cstep, const uint32_t *fstep, uint32_t *key, int32_t *idx,
-                                  int32_t *order_count) {
+                                  int32_t *order_count, const unsigned long long *move_list) {
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n == 0) *order_count = (int32_t)count;
     if (n >= count) return;
-    const Move mv = ctx_decode(c, mp, round, (uint64_t)(first + n));
+    const Move mv = move_list ? unpack_move(move_list[n]) : ctx_decode(c, mp, round, (uint64_t)(first + n));
     uint32_t d = ps::NEVER;
     if (mv.type == MOVE_SHIFT) {
         const int q = mv.a < mv.b ? mv.a : mv.b;
@@ -594,7 +596,7 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
     PS_CUDA(cudaMallocAsync((void **)&idx, (size_t)N * 4, s));
     PS_CUDA(cudaMallocAsync(&tmp, tmp_bytes, s));
     divergence_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N,
-                                                                 p.cstep, p.fstep, keys, idx, order);
+                                                                 p.cstep, p.fstep, keys, idx, order, p.move_list);
     PS_CUDA(cudaGetLastError());
     PS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, 32, s));
     cudaFreeAsync(keys, s);
@@ -953,7 +955,8 @@ int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
 }
 
 static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r,
-                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk);
+                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk,
+                           const int32_t *first_list = nullptr);
 
 int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r, void *stream) {
     NvtxRange nvtx("ps_eval_batch n=%llu", (unsigned long long)(b ? b->num_candidates : 0));
@@ -961,7 +964,8 @@ int ps_eval_batch(const ps_instance *I, const ps_cand_batch *b, const ps_result_
 }
 
 static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const ps_result_batch *r,
-                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk) {
+                           cudaStream_t stream, const int32_t *ready, int64_t ready_chunk,
+                           const int32_t *first_list) {
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
     if (b->num_candidates < 0) return fail(PS_ERR_INVALID, "negative candidate count");
     if (b->num_candidates == 0) return PS_OK;
@@ -998,7 +1002,7 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
     p.events_total = (unsigned long long *)r->events_total;
     p.ready = ready;
     p.ready_chunk = ready_chunk;
-    int rc = run_eval(I, p, false, stream, b->base);
+    int rc = run_eval(I, p, false, stream, b->base, first_list);
     if (rc) return rc;
     // Rows that are not permutations (the evaluator flags them malformed) are replayed with the
     // reference's literal semantics: they end in OrderInfeasible with its blocked stages
@@ -1017,11 +1021,13 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
 
 // One warp per (candidate, stage): copy the reference row; the stage-0 warp copies the mask.
 __global__ void delta_rows_kernel(int64_t N, int P, int stride, int mask_words, const uint16_t *ref,
-                                  const uint32_t *ref_mask, uint16_t *out, uint32_t *out_mask) {
+                                  const uint32_t *ref_mask, uint16_t *out, uint32_t *out_mask,
+                                  const unsigned long long *moves) {
     const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= N * P) return;
     const int64_t c = row / P;
+    if (moves && unpack_move(moves[c]).type != MOVE_GENERAL) return;    // (evaluated as a move)
     const int s = (int)(row % P);
     const uint32_t *src = reinterpret_cast<const uint32_t *>(ref + (size_t)s * stride);
     uint32_t *dst = reinterpret_cast<uint32_t *>(out + ((size_t)c * P + s) * stride);
@@ -1033,9 +1039,10 @@ __global__ void delta_rows_kernel(int64_t N, int P, int stride, int mask_words, 
 // One thread per candidate: apply its differences (after delta_rows_kernel, same stream).
 __global__ void delta_apply_kernel(int64_t N, int P, int stride, int mask_words, const uint32_t *doff,
                                    const uint32_t *diffs, const uint32_t *foff, const uint32_t *flips,
-                                   uint16_t *out, uint32_t *out_mask) {
+                                   uint16_t *out, uint32_t *out_mask, const unsigned long long *moves) {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
+    if (moves && unpack_move(moves[c]).type != MOVE_GENERAL) return;
     for (uint32_t k = doff[c]; k < doff[c + 1]; ++k) {
         const uint32_t e = diffs[2 * (size_t)k];
         out[((size_t)c * P + (e >> 16)) * stride + (e & 0xFFFFu)] = (uint16_t)diffs[2 * (size_t)k + 1];
@@ -1044,6 +1051,92 @@ __global__ void delta_apply_kernel(int64_t N, int P, int stride, int mask_words,
         const uint32_t b = flips[k];
         out_mask[(size_t)c * mask_words + (b >> 5)] ^= 1u << (b & 31);
     }
+}
+
+// Classify each delta-encoded candidate: one move of the reference structure —
+// SHIFT (the diffs are one stage's contiguous run of positions holding the reference run rotated by
+// one: the op at one end moved to the other), TOGGLE (one offloadable bit flipped) or NOOP — is
+// evaluated by the move-encoded search kernel against the reference (and its recorded base);
+// anything else is GENERAL (rebuilt in HBM and evaluated materialised), INVALID when an entry is
+// out of range (the call then fails).
+__global__ void delta_classify_kernel(MoveCtx c, int64_t N, uint64_t nd, uint64_t nf, int moves_ok,
+                                      const uint16_t *ref, const uint32_t *doff, const uint32_t *diffs,
+                                      const uint32_t *foff, const uint32_t *flips, unsigned long long *moves,
+                                      int32_t *general, int32_t *err) {
+    const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const uint32_t d0 = doff[n], d1 = doff[n + 1], f0 = foff[n], f1 = foff[n + 1];
+    Move mv;
+    mv.type = MOVE_GENERAL;
+    mv.stage = mv.a = mv.b = mv.mb = 0;
+    bool ok = d0 <= d1 && d1 <= nd && f0 <= f1 && f1 <= nf;
+    for (uint32_t k = d0; ok && k < d1; ++k) {
+        const uint32_t e = diffs[2 * (size_t)k];
+        if ((int)(e >> 16) >= c.P || (int)(e & 0xFFFFu) >= c.L) ok = false;
+    }
+    for (uint32_t k = f0; ok && k < f1; ++k)
+        if (flips[k] >= (uint32_t)(c.P * c.m)) ok = false;
+    if (!ok) {
+        mv.type = MOVE_INVALID;
+        atomicOr(err, 1);
+    } else if (moves_ok) {
+        const uint32_t nd_c = d1 - d0, nf_c = f1 - f0;
+        if (nd_c == 0 && nf_c == 0) {
+            mv.type = MOVE_NOOP;
+        } else if (nd_c == 0 && nf_c == 1) {
+            const int s = (int)(flips[f0] / (uint32_t)c.m), j = (int)(flips[f0] % (uint32_t)c.m);
+            if (ctx_offloadable(c, s, j)) { mv.type = MOVE_TOGGLE; mv.stage = s; mv.mb = j; }
+        } else if (nf_c == 0 && nd_c >= 2) {
+            const uint32_t e0 = diffs[2 * (size_t)d0];
+            const int s = (int)(e0 >> 16), lo = (int)(e0 & 0xFFFFu), hi = lo + (int)nd_c - 1;
+            bool run = hi < c.L;
+            for (uint32_t t = 0; run && t < nd_c; ++t) {
+                const uint32_t e = diffs[2 * (size_t)(d0 + t)];
+                run = (int)(e >> 16) == s && (int)(e & 0xFFFFu) == lo + (int)t;
+            }
+            if (run) {
+                const uint16_t *row = ref + (size_t)s * c.stride;
+                bool left = true, right = true;
+                for (uint32_t t = 0; t < nd_c; ++t) {
+                    const uint32_t code = diffs[2 * (size_t)(d0 + t) + 1];
+                    left = left && code == (uint32_t)(t + 1 < nd_c ? row[lo + t + 1] : row[lo]);
+                    right = right && code == (uint32_t)(t > 0 ? row[lo + t - 1] : row[hi]);
+                }
+                if (left || right) {
+                    mv.type = MOVE_SHIFT;
+                    mv.stage = s;
+                    mv.a = left ? lo : hi;
+                    mv.b = left ? hi : lo;
+                }
+            }
+        }
+    }
+    moves[n] = pack_move(mv);
+    if (mv.type == MOVE_GENERAL) general[1 + atomicAdd(general, 1)] = (int32_t)n;
+}
+
+// *flag = 0 if the two structures differ (the recorded base is not the delta batch's reference).
+__global__ void same_structure_kernel(const uint16_t *a, const uint16_t *b, int n16, const uint32_t *ma,
+                                      const uint32_t *mb, int nm, int32_t *flag) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n16; k += gridDim.x * blockDim.x)
+        if (a[k] != b[k]) *flag = 0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nm; k += gridDim.x * blockDim.x)
+        if (ma[k] != mb[k]) *flag = 0;
+}
+
+// The reference structure is a valid one (each stage row a permutation of its 3m ops), so its
+// moves need no validation.
+static bool valid_structure(const ps_instance *I, const uint16_t *ref) {
+    std::vector<unsigned char> seen((size_t)I->m * 3);
+    for (int i = 0; i < I->P; ++i) {
+        std::fill(seen.begin(), seen.end(), 0);
+        for (int q = 0; q < I->L; ++q) {
+            const uint32_t op = ref[(size_t)i * I->stride + q], j = op >> 2, k = op & 3u;
+            if (j >= (uint32_t)I->m || k > 2u || seen[j * 3 + k]) return false;
+            seen[j * 3 + k] = 1;
+        }
+    }
+    return true;
 }
 
 int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, const ps_result_batch *r, void *stream) {
@@ -1056,69 +1149,116 @@ int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, cons
     if (r->events_total) return fail(PS_ERR_INVALID, "events_total is a device counter: use ps_eval_batch");
     const uint64_t nd = b->diff_offset[N], nf = b->flip_offset[N];
     if ((nd && !b->diffs) || (nf && !b->flips)) return fail(PS_ERR_INVALID, "diffs / flips missing");
-    for (int64_t c = 0; c < N; ++c)
-        if (b->diff_offset[c + 1] < b->diff_offset[c] || b->flip_offset[c + 1] < b->flip_offset[c])
-            return fail(PS_ERR_INVALID, "offsets must be non-decreasing");
-    for (uint64_t k = 0; k < nd; ++k) {
-        const uint32_t e = b->diffs[2 * k];
-        if ((int)(e >> 16) >= I->P || (int)(e & 0xFFFFu) >= I->L) return fail(PS_ERR_INVALID, "diff %llu out of range", (unsigned long long)k);
-    }
-    for (uint64_t k = 0; k < nf; ++k)
-        if (b->flips[k] >= (uint32_t)(I->P * I->m)) return fail(PS_ERR_INVALID, "flip %llu out of range", (unsigned long long)k);
+    if (nd > 0xFFFFFFFFull || nf > 0xFFFFFFFFull) return fail(PS_ERR_RANGE, "at most 2^32-1 diffs and flips");
     DeviceGuard guard(I->device);
     if (!guard.ok) return fail(PS_ERR_CUDA, "cannot select device %d", I->device);
     cudaStream_t s = (cudaStream_t)stream;
-    // device arena: the encoded batch, then the rebuilt candidates and the outputs
+    // Candidates that are one move of the reference run on the move-encoded kernel (as search
+    // rounds do), when the reference is well formed, its incumbent copy fits in shared memory and no
+    // time can leave the evaluator's range (PS_FLAG_RANGE candidates need rows for the 64-bit pass).
+    const bool moves_ok = env_int("PS_DELTA_MOVES", 1) != 0 && I->time_safe == INT_MAX &&
+                          (size_t)incumbent_words(I, true) * 4 <= (size_t)I->max_smem_optin &&
+                          valid_structure(I, b->ref_orders);
+    // device arena: the encoded batch, the move list, the general list and flags, the rebuilt
+    // candidates, the outputs
     const size_t n_ref = (size_t)I->P * I->stride * 2, n_rmask = (size_t)I->mask_words * 4;
     const size_t n_off = (size_t)(N + 1) * 4, n_diff = (size_t)nd * 8, n_flip = (size_t)nf * 4;
     const size_t n_ord = (size_t)N * I->P * I->stride * 2, n_mask = (size_t)N * I->mask_words * 4;
     const size_t n_peak = r->peak ? (size_t)N * I->P * 8 : 0, n_blk = r->blocked ? (size_t)N * 4 : 0;
-    size_t sizes[13] = {n_ref, n_rmask, n_off, n_diff, n_off, n_flip, n_ord, n_mask, (size_t)N * 8, (size_t)N * 8,
-                        n_peak, (size_t)N * 4, n_blk};
-    size_t off[13], total = 0;
-    for (int k = 0; k < 13; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
+    enum { A_REF, A_RMASK, A_DOFF, A_DIFF, A_FOFF, A_FLIP, A_ORD, A_MASK, A_SPAN, A_BUB, A_PEAK, A_FLAGS, A_BLK,
+           A_MOVES, A_GEN, A_FLAG2, A_COUNT };
+    size_t sizes[A_COUNT] = {n_ref, n_rmask, n_off, n_diff, n_off, n_flip, n_ord, n_mask, (size_t)N * 8, (size_t)N * 8,
+                             n_peak, (size_t)N * 4, n_blk, (size_t)N * 8, (size_t)(N + 1) * 4, 8};
+    size_t off[A_COUNT], total = 0;
+    for (int k = 0; k < A_COUNT; ++k) { off[k] = total; total += (sizes[k] + 255) & ~(size_t)255; }
     char *arena = nullptr;
     PS_CUDA(cudaMallocAsync((void **)&arena, total, s));
     const void *srcs[6] = {b->ref_orders, b->ref_mask, b->diff_offset, b->diffs, b->flip_offset, b->flips};
     for (int k = 0; k < 6; ++k)
         if (sizes[k]) PS_CUDA(cudaMemcpyAsync(arena + off[k], srcs[k], sizes[k], cudaMemcpyHostToDevice, s));
-    uint16_t *ord = (uint16_t *)(arena + off[6]);
-    uint32_t *msk = (uint32_t *)(arena + off[7]);
-    const int64_t warps = N * I->P;
-    delta_rows_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
-        N, I->P, I->stride, I->mask_words, (const uint16_t *)(arena + off[0]), (const uint32_t *)(arena + off[1]), ord, msk);
-    delta_apply_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(
-        N, I->P, I->stride, I->mask_words, (const uint32_t *)(arena + off[2]), (const uint32_t *)(arena + off[3]),
-        (const uint32_t *)(arena + off[4]), (const uint32_t *)(arena + off[5]), ord, msk);
+    const uint16_t *ref_d = (const uint16_t *)(arena + off[A_REF]);
+    const uint32_t *rmask_d = (const uint32_t *)(arena + off[A_RMASK]);
+    unsigned long long *moves = (unsigned long long *)(arena + off[A_MOVES]);
+    int32_t *general = (int32_t *)(arena + off[A_GEN]);
+    int32_t *flags2 = (int32_t *)(arena + off[A_FLAG2]);       // [0] error, [1] base is the reference
+    PS_CUDA(cudaMemsetAsync(general, 0, 4, s));
+    const int32_t init2[2] = {0, 1};
+    PS_CUDA(cudaMemcpyAsync(flags2, init2, 8, cudaMemcpyHostToDevice, s));
+    delta_classify_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(
+        move_ctx(I), N, nd, nf, moves_ok ? 1 : 0, ref_d, (const uint32_t *)(arena + off[A_DOFF]),
+        (const uint32_t *)(arena + off[A_DIFF]), (const uint32_t *)(arena + off[A_FOFF]),
+        (const uint32_t *)(arena + off[A_FLIP]), moves, general, flags2);
     PS_CUDA(cudaGetLastError());
-    ps_cand_batch db;
-    memset(&db, 0, sizeof db);
-    db.num_candidates = N;
-    db.stage_orders = ord;
-    db.offload_mask = msk;
-    db.base = b->base;
-    db.order_bytes = 2;
+    const ps_base *B = b->base && b->base->inst == I ? b->base : nullptr;
+    if (B && moves_ok) {
+        same_structure_kernel<<<32, 256, 0, s>>>(ref_d, B->orders, I->P * I->stride, rmask_d, B->mask, I->mask_words,
+                                                 flags2 + 1);
+        PS_CUDA(cudaGetLastError());
+    }
     ps_result_batch dr = *r;
-    dr.makespan = (int64_t *)(arena + off[8]);
-    dr.bubble = (double *)(arena + off[9]);
-    dr.peak = n_peak ? (int64_t *)(arena + off[10]) : nullptr;
-    dr.flags = (uint32_t *)(arena + off[11]);
-    dr.blocked = n_blk ? (uint32_t *)(arena + off[12]) : nullptr;
+    dr.makespan = (int64_t *)(arena + off[A_SPAN]);
+    dr.bubble = (double *)(arena + off[A_BUB]);
+    dr.peak = n_peak ? (int64_t *)(arena + off[A_PEAK]) : nullptr;
+    dr.flags = (uint32_t *)(arena + off[A_FLAGS]);
+    dr.blocked = n_blk ? (uint32_t *)(arena + off[A_BLK]) : nullptr;
     dr.trace_code = nullptr;
     dr.trace_start = nullptr;
     dr.trace_stride = 0;
-    int rc = eval_batch_impl(I, &db, &dr, s, nullptr, 0);
+    int rc = PS_OK;
+    if (moves_ok) {
+        // pass 1: the move candidates (GENERAL / INVALID ones are skipped by the kernel)
+        EvalParams p;
+        memset(&p, 0, sizeof p);
+        fill_instance(I, &p);
+        p.N = N;
+        p.inc_orders = ref_d;
+        p.inc_mask = rmask_d;
+        p.move_list = moves;
+        p.base_valid = B ? flags2 + 1 : nullptr;
+        p.shift_permille = 1000;
+        p.max_shift = 1;
+        p.makespan = dr.makespan;
+        p.bubble = dr.bubble;
+        p.peak = dr.peak;
+        p.flags = dr.flags;
+        p.blocked = dr.blocked;
+        rc = run_eval(I, p, true, s, B);
+    }
+    if (rc == PS_OK) {
+        // pass 2: the general candidates, rebuilt in HBM and evaluated materialised
+        uint16_t *ord = (uint16_t *)(arena + off[A_ORD]);
+        uint32_t *msk = (uint32_t *)(arena + off[A_MASK]);
+        const int64_t warps = N * I->P;
+        delta_rows_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
+            N, I->P, I->stride, I->mask_words, ref_d, rmask_d, ord, msk, moves);
+        delta_apply_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(
+            N, I->P, I->stride, I->mask_words, (const uint32_t *)(arena + off[A_DOFF]),
+            (const uint32_t *)(arena + off[A_DIFF]), (const uint32_t *)(arena + off[A_FOFF]),
+            (const uint32_t *)(arena + off[A_FLIP]), ord, msk, moves);
+        PS_CUDA(cudaGetLastError());
+        ps_cand_batch db;
+        memset(&db, 0, sizeof db);
+        db.num_candidates = N;
+        db.stage_orders = ord;
+        db.offload_mask = msk;
+        db.base = b->base;
+        db.order_bytes = 2;
+        rc = eval_batch_impl(I, &db, &dr, s, nullptr, 0, general);
+    }
+    int32_t h_err = 0;
     if (rc == PS_OK) {
         PS_CUDA(cudaMemcpyAsync(r->makespan, dr.makespan, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
         PS_CUDA(cudaMemcpyAsync(r->bubble, dr.bubble, (size_t)N * 8, cudaMemcpyDeviceToHost, s));
         PS_CUDA(cudaMemcpyAsync(r->flags, dr.flags, (size_t)N * 4, cudaMemcpyDeviceToHost, s));
         if (n_peak) PS_CUDA(cudaMemcpyAsync(r->peak, dr.peak, n_peak, cudaMemcpyDeviceToHost, s));
         if (n_blk) PS_CUDA(cudaMemcpyAsync(r->blocked, dr.blocked, n_blk, cudaMemcpyDeviceToHost, s));
+        PS_CUDA(cudaMemcpyAsync(&h_err, flags2, 4, cudaMemcpyDeviceToHost, s));
     }
     cudaFreeAsync(arena, s);
     cudaError_t e = cudaStreamSynchronize(s);
     if (rc) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "ps_eval_batch_host_delta");
+    if (h_err) return fail(PS_ERR_INVALID, "a diff or flip entry (or offset) is out of range");
     return PS_OK;
 }
 

@@ -49,8 +49,10 @@ PS_HD Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
     return out;
 }
 
-// A decoded neighbour.  type NOOP leaves the incumbent unchanged.
-constexpr int MOVE_NOOP = 0, MOVE_SHIFT = 1, MOVE_TOGGLE = 2;
+// A decoded neighbour.  type NOOP leaves the incumbent unchanged.  In explicit move lists
+// (delta-encoded batches) GENERAL marks a candidate that is not one move of the reference
+// structure (evaluated materialised) and INVALID one whose encoding is out of range.
+constexpr int MOVE_NOOP = 0, MOVE_SHIFT = 1, MOVE_TOGGLE = 2, MOVE_GENERAL = 3, MOVE_INVALID = 4;
 
 struct Move {
     int type;
@@ -58,6 +60,21 @@ struct Move {
     int a, b;    // SHIFT: the op at position a moves to position b
     int mb;      // TOGGLE: microbatch whose F activation flips its offload bit
 };
+
+// Explicit move lists: type:4 | stage:8 | a:16 | b:16 | mb:16 in one 64-bit word.
+PS_HD uint64_t pack_move(const Move &mv) {
+    return (uint64_t)(uint32_t)mv.type | ((uint64_t)(uint32_t)mv.stage << 4) | ((uint64_t)(uint32_t)mv.a << 12) |
+           ((uint64_t)(uint32_t)mv.b << 28) | ((uint64_t)(uint32_t)mv.mb << 44);
+}
+PS_HD Move unpack_move(uint64_t w) {
+    Move mv;
+    mv.type = (int)(w & 0xFu);
+    mv.stage = (int)((w >> 4) & 0xFFu);
+    mv.a = (int)((w >> 12) & 0xFFFFu);
+    mv.b = (int)((w >> 28) & 0xFFFFu);
+    mv.mb = (int)((w >> 44) & 0xFFFFu);
+    return mv;
+}
 
 // offloadable(stage, mb) is supplied by the caller (act_size > 0).
 template <typename Offloadable>

@@ -62,6 +62,9 @@ struct EvalParams {
     uint64_t seed, round;
     int64_t first_index;
     uint32_t shift_permille, max_shift;
+    const unsigned long long *move_list;   // explicit moves per candidate (pack_move), else Philox
+    const int32_t *base_valid;             // optional device flag: 0 = the recorded base is not the
+                                           // incumbent (no prefix sharing)
     // outputs
     int64_t *makespan;
     double *bubble;
@@ -688,7 +691,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         top = (V)*reinterpret_cast<const long long *>(rg + 14);
         peak = (V)*reinterpret_cast<const long long *>(rg + 16);
     };
-    const int n_ck = (p.ck && !REC) ? p.base_info[0] : 0;
+    const int n_ck = (p.ck && !REC && (!p.base_valid || *p.base_valid)) ? p.base_info[0] : 0;
     // Checkpoints to resume from: the base's for a candidate; for a re-recording (REC with
     // rec_prev) those of the previous base, whose prefix the new one shares up to their divergence.
     const int n_src = REC ? (p.rec_prev ? p.base_info[0] : 0) : n_ck;
@@ -1013,8 +1016,16 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         }
         if (MOVES) {
             uint64_t gidx = (uint64_t)(p.first_index + cand);
-            mv = decode_move(p.seed, p.round, gidx, P, m, p.shift_permille, p.max_shift, p.any_off != 0,
-                             [&](int s, int j) { return ldv<V>(p.vals, (UNI ? s : s * m + j) * 4 + 3) > V(0); });
+            if (p.move_list) {
+                mv = unpack_move(p.move_list[cand]);
+                if (mv.type >= MOVE_GENERAL) {          // (warp-uniform) evaluated by another pass
+                    __syncwarp();
+                    continue;
+                }
+            } else {
+                mv = decode_move(p.seed, p.round, gidx, P, m, p.shift_permille, p.max_shift, p.any_off != 0,
+                                 [&](int s, int j) { return ldv<V>(p.vals, (UNI ? s : s * m + j) * 4 + 3) > V(0); });
+            }
         }
         __syncwarp();
         bool bad = false;

@@ -199,3 +199,92 @@ def test_delta_encoded_host_batch_equals_the_full_rows(cuda_ok):
                 assert (getattr(got, f) == getattr(want, f)).all(), (cfg, f)
             ok = want.flags == 1
             assert (got.bubble[ok] == want.bubble[ok]).all()
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_delta_batch_moves_and_general_candidates(cuda_ok, cfg):
+    """ps_eval_batch_host_delta evaluates a candidate that is one move of the reference (a shift's
+    rotated run, one offloadable bit, nothing) on the move-encoded kernel and anything else
+    materialised.  A batch mixing search neighbours with two-move candidates, wider
+    rotations, unsorted entries, a shift plus a flip and malformed rows gives exactly the full-row
+    outputs without a base — with the reference's recorded base, with no base, and with a base
+    recorded on another structure; an out-of-range entry fails the call."""
+    import torch
+    from paper_2510_05186_b200 import _native as N
+    from paper_2510_05186_b200.engine import Base
+    from paper_2510_05186_b200.packing import delta_encode
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200 import workloads
+    inst = workloads.CONFIGS[cfg]()
+    s0, _ = best_feasible(inst)
+    ls = LocalSearch(inst, {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}, s0.offloaded,
+                     SearchConfig(seed=3, neighbours=512, shift_permille=700, max_shift=4))
+    di, pk = ls.di, ls.di.packed
+    n = 512 if cfg != 5 else 128
+    o, mk = ls.materialize(0, n, 0)
+    o = o.cpu().numpy().view(np.uint16).copy()
+    mk = mk.cpu().numpy().view(np.uint32).copy()
+    ref_o = ls.inc_orders.cpu().numpy().view(np.uint16).copy()
+    ref_m = ls.inc_mask.cpu().numpy().view(np.uint32).copy()
+    rng = np.random.default_rng(cfg)
+    L = 3 * pk.num_microbatches
+    extra_o, extra_m = [], []
+    for k in range(48):
+        a, b = o[k].copy(), mk[k].copy()
+        kind = k % 6
+        if kind == 0:                       # two moves: this neighbour's and the next one's
+            a2 = o[k + 1]
+            d = a2 != ref_o
+            a[d] = a2[d]
+            b ^= mk[k + 1] ^ ref_m
+        elif kind == 1:                     # a run rotated by two (not a single move)
+            s, q = int(rng.integers(pk.num_stages)), int(rng.integers(L - 3))
+            a = ref_o.copy()
+            a[s, q:q + 3] = np.roll(ref_o[s, q:q + 3], 2)
+            b = ref_m.copy()
+        elif kind == 2:                     # a shift and a flipped bit together
+            s = int(rng.integers(pk.num_stages))
+            a = ref_o.copy()
+            a[s, 5:7] = ref_o[s, 5:7][::-1]
+            b = ref_m.copy()
+            b[0] ^= 1
+        elif kind == 3:                     # a repeated op (malformed: literal replay)
+            s = int(rng.integers(pk.num_stages))
+            a = ref_o.copy()
+            a[s, 4] = a[s, 3]
+            b = ref_m.copy()
+        elif kind == 4:                     # swap of two far positions in one stage
+            s = int(rng.integers(pk.num_stages))
+            a = ref_o.copy()
+            a[s, [2, 9]] = a[s, [9, 2]]
+            b = ref_m.copy()
+        else:                               # two flipped bits
+            a = ref_o.copy()
+            b = ref_m.copy()
+            b[0] ^= 3
+        extra_o.append(a)
+        extra_m.append(b)
+    orders = np.concatenate([o, np.stack(extra_o)])
+    masks = np.concatenate([mk, np.stack(extra_m)])
+    want = di.evaluate_host(orders, masks, peak=True, base=None)
+    doff, diffs, foff, flips = delta_encode(ref_o, ref_m, orders, masks)
+    # the same entries in reverse order within each candidate (unsorted: not classified as moves)
+    diffs_rev = diffs.copy()
+    for c in range(0, len(orders), 7):
+        diffs_rev[doff[c]:doff[c + 1]] = diffs[doff[c]:doff[c + 1]][::-1]
+    other = Base(di)
+    other.record(torch.from_numpy(orders[n + 4].view(np.int16)).cuda(), torch.from_numpy(masks[n + 4].view(np.int32)).cuda())
+    for bb in (ls.base, None, other):
+        for dd in (diffs, diffs_rev):
+            got = di.evaluate_host_delta(ref_o, ref_m, doff, dd, foff, flips, peak=True, base=bb)
+            for f in ("flags", "makespan", "peak", "blocked"):
+                assert (getattr(got, f) == getattr(want, f)).all(), (cfg, f, bb is None)
+            ok = want.flags == 1
+            assert (got.bubble[ok] == want.bubble[ok]).all()
+    assert (want.flags == 1).any() and (want.flags == 2).any()
+    bad = diffs.copy()
+    bad[int(doff[3]), 0] = (pk.num_stages << 16)           # stage out of range
+    with pytest.raises(N.NativeError):
+        di.evaluate_host_delta(ref_o, ref_m, doff, bad, foff, flips, peak=True, base=ls.base)
