@@ -786,6 +786,31 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
     // scheduler is translation invariant on such states — every start is a max of live times plus
     // constants, every commit adds a constant, the fold line moves with them — so the candidate
     // continues as the base does, `delta` later.
+    bool rec_chg = false;        // REC: this stage's offload bits differ from the previous base's
+    int rec_dn = 0;              // REC: and its count of offloaded activations by this much
+    // A recording's suffix peaks: walking c from `hi` down to 0, rg[18] of checkpoint c = run, then
+    // run = max(run, rg[10]) (the peak folded in c's interval); eight loads in flight per batch.
+    auto suffix_peaks = [&](int hi, long long run) {
+        constexpr int U = 8;
+        int c = hi;
+        for (; c - (U - 1) >= 0; c -= U) {
+            long long sg[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                sg[u] = *reinterpret_cast<const long long *>(p.ck + (size_t)(c - u) * p.ck_words + ck_r + lane * CK_REGW + 10);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                *reinterpret_cast<long long *>(p.ck + (size_t)(c - u) * p.ck_words + ck_r + lane * CK_REGW + 18) = run;
+                run = sg[u] > run ? sg[u] : run;
+            }
+        }
+        for (; c >= 0; --c) {
+            uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
+            const long long sg = *reinterpret_cast<const long long *>(rg + 10);
+            *reinterpret_cast<long long *>(rg + 18) = run;
+            run = sg > run ? sg : run;
+        }
+    };
     int conv_delta = 0;
     auto same_state = [&](int c) -> bool {
         const uint32_t *src = p.ck + (size_t)c * p.ck_words;
@@ -1234,20 +1259,41 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
                 int nb = 0;
                 for (int w = 0; w < MW; ++w) nb += __popc(SB(o_offm + (w)));
                 n_unrel += cand_unrel - nb;
+                if (REC) {
+                    // did this stage's offload bits change from the previous base's (restored above)?
+                    bool chg = false;
+                    for (int w = 0; w < MW; ++w) {
+                        const int gb = i * m + w * 32, q = gb >> 5, sh = gb & 31, mwords = (P * m + 31) / 32;
+                        uint32_t bits = (q < mwords ? __ldcg(&p.masks[(size_t)cand * mwords + q]) : 0u) >> sh;
+                        if (sh && q + 1 < mwords) bits |= __ldcg(&p.masks[(size_t)cand * mwords + q + 1]) << (32 - sh);
+                        const int nbits = m - w * 32;
+                        if (nbits < 32) bits &= (1u << nbits) - 1u;
+                        chg = chg || bits != SB(o_offm + (w));
+                    }
+                    rec_chg = chg;
+                    rec_dn = cand_unrel - nb;
+                }
                 build_mask(false);
                 if (wmask_on) {
                     pwm = 0;
                     for (int w = 0; w < MW; ++w)
                         pwm |= (SB(o_poff + (w)) ? 1u << w : 0u) | (SB(o_prel + (w)) ? 1u << (16 + w) : 0u);
                 }
-                if (REC) {
-                    // the kept checkpoints become the new base's: its offload bits, and the
-                    // outstanding-transfer count that goes with them (the suffix-sharing compare
-                    // reads both)
-                    for (int c = 0; c <= ck_idx; ++c) {
+            }
+            if (REC) {
+                // The kept checkpoints become the new base's: its offload bits, and the
+                // outstanding-transfer count that goes with them (the suffix-sharing compare reads
+                // both) — only for the stages whose bits changed (none after a shift), with the
+                // lanes striding over the checkpoints so their loads overlap.
+                const int dn = has_stage ? rec_dn : 0;
+                __syncwarp();
+                for (unsigned chg = __ballot_sync(0xffffffffu, has_stage && rec_chg); chg; chg &= chg - 1) {
+                    const int st = __ffs(chg) - 1;
+                    const int dns = __shfl_sync(0xffffffffu, dn, st);
+                    for (int c = lane; c <= ck_idx; c += 32) {
                         uint32_t *dst = p.ck + (size_t)c * p.ck_words;
-                        for (int w = 0; w < MW; ++w) dst[2 * P * m + i * MW + w] = SB(o_offm + (w));
-                        dst[ck_r + lane * CK_REGW + 7] += (uint32_t)(cand_unrel - nb);
+                        for (int w = 0; w < MW; ++w) dst[2 * P * m + st * MW + w] = SB(o_bits + st * MW + w);
+                        if (dns) dst[ck_r + st * CK_REGW + 7] += (uint32_t)dns;
                     }
                 }
             }
@@ -1517,13 +1563,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
                 p.base_res[2 + P + i] = hi;
                 p.base_res[2 + 2 * P + i] = fs;
                 // suffix peaks of the checkpoints up to conv_c (later ones are unchanged)
-                long long run = (long long)sfx;
-                for (int c = conv_c; c >= 0; --c) {
-                    uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
-                    const long long sg = *reinterpret_cast<const long long *>(rg + 10);
-                    *reinterpret_cast<long long *>(rg + 18) = run;
-                    run = sg > run ? sg : run;
-                }
+                suffix_peaks(conv_c, (long long)sfx);
             }
             const int old_win = p.base_info[4], old_events = p.base_info[2];
             __syncwarp();
@@ -1611,13 +1651,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
             }
             if (!unusable && has_stage) {
                 // S_c = max usage folded after checkpoint c (a converging candidate's peak suffix)
-                long long run = (long long)segpk;
-                for (int c = cc > 0 ? (cc - 1) / p.ck_interval : -1; c >= 0; --c) {
-                    uint32_t *rg = p.ck + (size_t)c * p.ck_words + ck_r + lane * CK_REGW;
-                    const long long sg = *reinterpret_cast<const long long *>(rg + 10);
-                    *reinterpret_cast<long long *>(rg + 18) = run;
-                    run = sg > run ? sg : run;
-                }
+                suffix_peaks(cc > 0 ? (cc - 1) / p.ck_interval : -1, (long long)segpk);
             }
             if (lane == 0) {
                 p.base_info[5] = -1;                      // no shifted suffix to apply
