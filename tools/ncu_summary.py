@@ -1,6 +1,6 @@
 """Summarise an ncu --set full capture of the evaluator plus the launch list of a bench run.
 
-  python tools/ncu_summary.py <full.ncu-rep> <launches.csv> <out.json> "<command>"
+  python tools/ncu_summary.py <full.ncu-rep> <launches.csv> <out.json> "<command>" [round]
 """
 import csv
 import io
@@ -10,6 +10,7 @@ import sys
 from collections import defaultdict
 
 rep, launches, out, command = sys.argv[1:5]
+rnd = int(sys.argv[5]) if len(sys.argv) > 5 else 2
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, v = rows[0], rows[1], rows[2]
@@ -30,7 +31,7 @@ def num(name):
 
 dur_ms = num("gpu__time_duration.sum")
 summary = {
-    "round": 1,
+    "round": rnd,
     "command": command,
     "kernel": get("Kernel Name") or get("Function Name"),
     "launch": {"grid": num("launch__grid_size"), "block": num("launch__block_size"),
