@@ -118,34 +118,92 @@ def generator_structures(inst, params: AdaParams = AdaParams()):
     ]
 
 
+def _row_codes(m: int, fill: int) -> "np.ndarray":
+    """filled_order's op codes ((microbatch - 1) << 2 | kind), the same for every stage."""
+    import numpy as np
+    codes = [(j << 2) | 0 for j in range(fill)]
+    for k in range(m):
+        codes += [(k << 2) | 1, (k << 2) | 2]
+        if fill + k < m:
+            codes.append(((fill + k) << 2) | 0)
+    return np.asarray(codes, np.uint16)
+
+
 def generate_all(inst: PipelineInstance, params: AdaParams = AdaParams(), device=None) -> dict:
-    """Every generator's schedule (or InfeasibleSchedule) from one batched evaluation."""
+    """Every generator's schedule (or InfeasibleSchedule) from one batched evaluation.
+
+    The whole AdaOffload back-off sequence (738 structures at 32 x 256) is encoded from one row per
+    fill value (filled_order does not depend on the stage) and evaluated in one launch without
+    traces; only the structures that become answers — AdaOffload's first feasible entry and the
+    other three generators — are re-run with their traces and decoded into Schedules."""
+    import numpy as np
+    import torch
+    from .engine import device_instance
     from .listsched import OrderInfeasible, run_orders
     P, m = inst.num_stages, inst.num_microbatches
     everything = frozenset(inst.offloadable_ops())
     backoff = ada_backoff_sequence(inst, params.tolerance)
-    cands = [({i: filled_order(inst, i, f[i]) for i in range(1, P + 1)}, everything) for f in backoff]
-    n_ada = len(cands)
-    cands.append(({i: filled_order(inst, i, 1) for i in range(1, P + 1)}, everything))
-    cands.append(({i: filled_order(inst, i, min(P - i + 1, m)) for i in range(1, P + 1)}, frozenset()))
+    fill_sets = [f for f in backoff] + [{i: 1 for i in range(1, P + 1)},
+                                        {i: min(P - i + 1, m) for i in range(1, P + 1)}]
+    n_ada = len(backoff)
+    di = device_instance(inst, device)
+    pk = di.packed
+    n = len(fill_sets) + 1
+    orders = np.zeros((n, P, pk.order_stride), np.uint16)
+    masks = np.zeros((n, pk.mask_words), np.uint32)
+    rows = {}
+    for c, f in enumerate(fill_sets):
+        for i in range(1, P + 1):
+            r = rows.get(f[i])
+            if r is None:
+                r = rows[f[i]] = _row_codes(m, f[i])
+            orders[c, i - 1, :3 * m] = r
+    seq_row = np.asarray([(j << 2) | k for j in range(m) for k in range(3)], np.uint16)
+    orders[n - 1, :, :3 * m] = seq_row
+    for op in everything:
+        b = (op[0] - 1) * m + (op[1] - 1)
+        masks[:n - 2, b >> 5] |= np.uint32(1 << (b & 31))          # ada and pipeoffload offload everything
+    dev = torch.device("cuda", di.device)
+    res = di.evaluate(torch.from_numpy(orders.view(np.int16)).to(dev), torch.from_numpy(masks.view(np.int32)).to(dev),
+                      peak=False)
+    flags = res.flags.cpu().numpy()
+    blocked = res.blocked.cpu().numpy()
+
+    def stages_of(c):
+        return [i + 1 for i in range(P) if (int(blocked[c]) >> i) & 1]
+
+    ada_idx = next((c for c in range(n_ada) if flags[c] & 1), None)
+    picks = {"ada": ada_idx, "pipeoffload": n_ada, "1f1b": n_ada + 1, "sequential": n_ada + 2}
+    structs = {}
+    for name, c in picks.items():
+        if c is None or not flags[c] & 1:
+            continue
+        if name == "sequential":
+            structs[name] = ({i: sequential_order(inst, i) for i in range(1, P + 1)}, frozenset())
+        else:
+            f = fill_sets[c]
+            structs[name] = ({i: filled_order(inst, i, f[i]) for i in range(1, P + 1)},
+                             frozenset() if name == "1f1b" else everything)
+    names = list(structs)
+    decoded = dict(zip(names, run_orders(inst, [structs[k] for k in names], device=device)))
     seq_ok = all(inst.mem_delta[OpId(i, j, F)] <= inst.mem_limit[i]
                  for i in range(1, P + 1) for j in range(1, m + 1))
-    cands.append(({i: sequential_order(inst, i) for i in range(1, P + 1)}, frozenset()))
-    res = run_orders(inst, cands, device=device)
     out = {}
-    ada = next((r for r in res[:n_ada] if not isinstance(r, OrderInfeasible)), None)
-    out["ada"] = ada if ada is not None else InfeasibleSchedule(
-        f"offload-everything exceeds memory (blocked stages: {list(res[n_ada - 1].stages)})")
-    po, fb, sq = res[n_ada:]
-    out["pipeoffload"] = po if not isinstance(po, OrderInfeasible) else InfeasibleSchedule(
-        f"offload-everything exceeds memory (blocked stages: {list(po.stages)})")
-    out["1f1b"] = fb if not isinstance(fb, OrderInfeasible) else InfeasibleSchedule(
-        f"1F1B exceeds memory (blocked stages: {list(fb.stages)})")
-    if not seq_ok:
-        out["sequential"] = InfeasibleSchedule("a stage cannot hold one activation")
-    else:
-        out["sequential"] = sq if not isinstance(sq, OrderInfeasible) else InfeasibleSchedule(
-            f"sequential blocked (stages {list(sq.stages)})")
+    for name in GENERATOR_ORDER:
+        got = decoded.get(name)
+        if name == "sequential" and not seq_ok:
+            out[name] = InfeasibleSchedule("a stage cannot hold one activation")
+            continue
+        if got is not None and not isinstance(got, OrderInfeasible):
+            out[name] = got
+            continue
+        c = picks[name] if name != "ada" else n_ada - 1
+        if name == "ada" or name == "pipeoffload":
+            out[name] = InfeasibleSchedule(f"offload-everything exceeds memory (blocked stages: {stages_of(c)})")
+        elif name == "1f1b":
+            out[name] = InfeasibleSchedule(f"1F1B exceeds memory (blocked stages: {stages_of(c)})")
+        else:
+            out[name] = InfeasibleSchedule(f"sequential blocked (stages {stages_of(c)})")
     return out
 
 
