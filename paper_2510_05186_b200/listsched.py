@@ -45,20 +45,27 @@ def channel_order_of(s, inst, channel: int) -> tuple:
 
 
 def _events_from_trace(pk, codes, starts, count, types):
-    """Rebuild commit-ordered events from the kernel trace (include/pipesched_b200.h)."""
-    compute, transfers = [], []
+    """Rebuild commit-ordered events from the kernel trace (include/pipesched_b200.h): the fields
+    are decoded with numpy, the event objects built in one pass."""
     Reload, Offload = types.TransferKind.RELOAD, types.TransferKind.OFFLOAD
     Op, Kind = getattr(types, "OpId", OpId), getattr(types, "OpKind", OpKind)   # the caller's op types
-    for q in range(count):
-        code = int(codes[q]) & 0xFFFFFFFF
-        t = int(starts[q])
-        rank, i0, j0, k = code >> 30, (code >> 24) & 63, (code >> 2) & 0x3FFFFF, code & 3
-        op = Op(i0 + 1, j0 + 1, Kind(k))
-        if rank == 0:
-            compute.append(types.ComputeEvent(op, t, t + int(pk.proc_time[i0, j0, k])))
+    code = np.asarray(codes[:count]).astype(np.uint32)
+    t = np.asarray(starts[:count]).astype(np.int64)
+    rank = code >> 30
+    i0 = ((code >> 24) & 63).astype(np.int64)
+    j0 = ((code >> 2) & 0x3FFFFF).astype(np.int64)
+    k = (code & 3).astype(np.int64)
+    comp = rank == 0
+    end = t + np.where(comp, pk.proc_time[i0, j0, np.where(comp, k, 0)], pk.offload_time)
+    kinds = [Kind(x) for x in range(3)]
+    compute, transfers = [], []
+    CE, TE = types.ComputeEvent, types.TransferEvent
+    for r, a, b, kk, s0, e0 in zip(rank.tolist(), i0.tolist(), j0.tolist(), k.tolist(), t.tolist(), end.tolist()):
+        op = Op(a + 1, b + 1, kinds[kk])
+        if r == 0:
+            compute.append(CE(op, s0, e0))
         else:
-            transfers.append(types.TransferEvent(op, Reload if rank == 1 else Offload,
-                                                 t, t + pk.offload_time))
+            transfers.append(TE(op, Reload if r == 1 else Offload, s0, e0))
     return compute, transfers
 
 
