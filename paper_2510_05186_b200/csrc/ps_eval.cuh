@@ -268,6 +268,9 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #ifndef PS_MIN_BLOCKS_G
 #define PS_MIN_BLOCKS_G 1     // global-memory state: one 16-warp block per SM, 122 registers (r01 A/B)
 #endif
+#ifndef PS_MIN_BLOCKS_NB
+#define PS_MIN_BLOCKS_NB 7    // materialised candidates without a base: full simulations (r02 A/B: 7 is -10% vs 5)
+#endif
 #ifndef PS_MIN_BLOCKS_MAT
 #define PS_MIN_BLOCKS_MAT 5   // materialised candidates: 102-register cap (r01 A/B)
 #endif
@@ -280,10 +283,16 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 
 // DERIVED: greedy channel mode (no explicit channel orders); UNI: microbatch-symmetric tables.
 // GS: per-candidate state in shared memory (0), in global scratch (1), in global scratch with
-// nonzero-word masks over the pending-transfer sets (2: many bitset words per stage, config 5).
+// nonzero-word masks over the pending-transfer sets (2: many bitset words per stage, config 5),
+// in shared memory without a recorded base (3: materialised full simulations; no checkpoint code,
+// built for 7 blocks per SM like the move-encoded kernel).
 template <typename V, bool MOVES, int GS, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 : GS ? PS_MIN_BLOCKS_G : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT)) eval_kernel(const EvalParams p) {
-    constexpr bool GSTATE = GS != 0;
+__global__ void __launch_bounds__((GS == 1 || GS == 2) ? 32 * PS_GSTATE_MAX_WARPS : 128,
+                                  REC ? 1 : (GS == 1 || GS == 2) ? PS_MIN_BLOCKS_G
+                                  : GS == 3 ? PS_MIN_BLOCKS_NB : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT))
+eval_kernel(const EvalParams p) {
+    constexpr bool GSTATE = GS == 1 || GS == 2;
+    constexpr bool NOBASE = GS == 3;
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;
@@ -691,7 +700,7 @@ __global__ void __launch_bounds__(GS ? 32 * PS_GSTATE_MAX_WARPS : 128, REC ? 1 :
         top = (V)*reinterpret_cast<const long long *>(rg + 14);
         peak = (V)*reinterpret_cast<const long long *>(rg + 16);
     };
-    const int n_ck = (p.ck && !REC && (!p.base_valid || *p.base_valid)) ? p.base_info[0] : 0;
+    const int n_ck = (!NOBASE && p.ck && !REC && (!p.base_valid || *p.base_valid)) ? p.base_info[0] : 0;
     // Checkpoints to resume from: the base's for a candidate; for a re-recording (REC with
     // rec_prev) those of the previous base, whose prefix the new one shares up to their divergence.
     const int n_src = REC ? (p.rec_prev ? p.base_info[0] : 0) : n_ck;

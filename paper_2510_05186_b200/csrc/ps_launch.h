@@ -16,6 +16,7 @@ struct Variant {
     bool derived;   // greedy channel mode
     bool uni;       // microbatch-symmetric instance tables
     bool wmask;     // (global state) nonzero-word masks over the pending-transfer sets
+    bool nobase;    // (materialised, shared-memory state) no recorded base: the full-simulation build
 };
 
 // One translation unit per (ledger value type V, move-encoded candidates).
