@@ -57,6 +57,21 @@ def test_one_and_two_ranks_follow_the_same_trajectory(cuda_ok, tmp_path, kick_mo
             assert d[key] == ref[key], (key, d["rank"])
 
 
+@pytest.mark.timeout(1500)
+def test_identical_best_schedule_at_1_2_4_8_ranks(cuda_ok, tmp_path):
+    """BASELINE's "identical best schedule for equal search budgets" at 1, 2, 4 and 8 ranks
+    (gloo, all on cuda:0): config 3, 8,192 neighbours per round in total, 16 descent rounds —
+    every rank of every world size holds the same improvement trail and best structure."""
+    runs = {w: _run_world(tmp_path, w, 3, 8192, 16, port=29571 + w) for w in (1, 2, 4, 8)}
+    ref = runs[1][0]
+    assert len(ref["trail"]) >= 5
+    for w, docs in runs.items():
+        assert [(d["first"], d["count"]) for d in docs] == [(k * 8192 // w, 8192 // w) for k in range(w)]
+        for d in docs:
+            for key in ("trail", "best", "rounds", "orders", "mask"):
+                assert d[key] == ref[key], (w, key, d["rank"])
+
+
 def test_sharded_round_through_the_c_abi_with_an_nccl_communicator(cuda_ok):
     """ps_search_round_sharded with the ncclComm_t of a one-rank NCCL group: the all-reduce(MIN)
     inside the C ABI call leaves the round's key as ps_search_round computes it."""
