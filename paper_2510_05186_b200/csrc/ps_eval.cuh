@@ -667,8 +667,9 @@ eval_kernel(const EvalParams p) {
                                       : __longlong_as_double(0x7ff8000000000000LL);
         if (p.blocked) p.blocked[cand] = blocked_mask;
 #ifdef PS_DEBUG_EVENTS
-        // diagnostics build: simulated events | restored-from step << 16 in place of blocked
-        if (p.blocked) p.blocked[cand] = (uint32_t)(ecount - ecount0) | ((uint32_t)min(ecount0, 32767) << 16);
+        // diagnostics build: simulated events | restored-from step << 16 in place of the bubble
+        // (tools/event_stats.py; early deadlock detection stays on without a blocked output)
+        if (p.bubble) p.bubble[cand] = (double)((uint32_t)(ecount - ecount0) | ((uint32_t)min(ecount0, 32767) << 16));
 #endif
     };
 

@@ -18,6 +18,11 @@ s0, _ = best_feasible(inst)
 orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
 n = 8192
 ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=n, shift_permille=700, max_shift=4))
+if os.environ.get("KVAR_INCUMBENT"):
+    z = np.load(os.environ["KVAR_INCUMBENT"])
+    ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
+    ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
+    ls.base.record(ls.inc_orders, ls.inc_mask)
 o, mk = ls.materialize(0, n, 0)
 r = ls.di.evaluate(o, mk, base=ls.base, out=ls.di.alloc_results(n, peak=False, blocked=False))
 torch.cuda.synchronize()
