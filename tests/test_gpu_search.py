@@ -372,7 +372,19 @@ SANITIZER_SCRIPT = (
     "ho = od.cpu().numpy().view(np.uint16).copy()\n"
     "ho[1, 0, 1] = ho[1, 0, 0]\n"                 # a repeated op: the literal replay pass
     "ls.di.evaluate_host(ho.astype(np.uint8), md.cpu().numpy(), base=ls.base)\n"
+    "ls.di.evaluate_host(ho.astype(np.uint8), md.cpu().numpy(), base=None)\n"      # full-simulation build
+    "from paper_2510_05186_b200.packing import delta_encode\n"                     # delta batch: moves + general
+    "ro, rm = ls.inc_orders.cpu().numpy().view(np.uint16), ls.inc_mask.cpu().numpy().view(np.uint32)\n"
+    "ls.di.evaluate_host_delta(ro, rm, *delta_encode(ro, rm, ho, md.cpu().numpy()), base=ls.base)\n"
     "print(lower_bounds(inst, [(0, {i: 0 for i in range(1, inst.num_stages + 1)}, {})]))\n"
+    "for c, n in ((4, 64), (5, 32)):\n"                                              # global-state kernels
+    "    i2 = workloads.CONFIGS[c]()\n"
+    "    s2, _ = best_feasible(i2)\n"
+    "    l2 = LocalSearch(i2, {i: stage_order_of(s2, i) for i in range(1, i2.num_stages + 1)}, s2.offloaded,\n"
+    "                     SearchConfig(seed=1, neighbours=n))\n"
+    "    l2.run(rounds=2)\n"
+    "from paper_2510_05186_b200 import make_uniform_instance\n"                    # 64-bit completion
+    "best_feasible(make_uniform_instance(4, 8, 20000000, 20000000, 20000000, 5, 1000, 2, 4))\n"
 )
 
 
