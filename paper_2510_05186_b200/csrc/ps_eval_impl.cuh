@@ -57,6 +57,7 @@ static cudaError_t occ_one(int block, size_t smem, int *n) {
         return v.uni ? FN<V, MOVES, 0, false, true, true> ARGS : FN<V, MOVES, 0, false, true, false> ARGS; \
     }                                                                                                 \
     if (v.gstate) return v.uni ? FN<V, false, 1, false, false, true> ARGS : FN<V, false, 1, false, false, false> ARGS; \
+    if (v.nobase) return v.uni ? FN<V, false, 3, false, false, true> ARGS : FN<V, false, 3, false, false, false> ARGS; \
     return v.uni ? FN<V, false, 0, false, false, true> ARGS : FN<V, false, 0, false, false, false> ARGS;
 
 #define PS_PICK_OCC(FN, ARGS)                                                                          \
@@ -67,6 +68,7 @@ static cudaError_t occ_one(int block, size_t smem, int *n) {
         return v.uni ? FN<V, MOVES, 0, true, true> ARGS : FN<V, MOVES, 0, true, false> ARGS; \
     }                                                                                                 \
     if (v.gstate) return v.uni ? FN<V, false, 1, false, true> ARGS : FN<V, false, 1, false, false> ARGS; \
+    if (v.nobase) return v.uni ? FN<V, false, 3, false, true> ARGS : FN<V, false, 3, false, false> ARGS; \
     return v.uni ? FN<V, false, 0, false, true> ARGS : FN<V, false, 0, false, false> ARGS;
 
 template <typename V, bool MOVES>
