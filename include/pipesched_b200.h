@@ -191,6 +191,12 @@ int ps_instance_get_info(const ps_instance *inst, ps_instance_info *out);
 int ps_base_create(const ps_instance *inst, ps_base **out);
 int ps_base_destroy(ps_base *base);
 int ps_base_record(ps_base *base, const uint16_t *orders, const uint32_t *mask, void *stream);
+/* The same for a candidate with explicit channel orders (device [G][chan_stride], ps_cand_batch
+   encoding): explicit-channel batches of that width (ps_eval_batch with channel_orders,
+   ps_search_round_explicit with desc->base) then resume from its checkpoints and converge onto it,
+   as derived-mode batches do with ps_base_record. */
+int ps_base_record_explicit(ps_base *base, const uint16_t *orders, const uint32_t *mask,
+                            const uint32_t *chan_orders, int32_t chan_stride, void *stream);
 /* Inspection (tests, diagnostics): copy one recorded table to host memory after synchronising.
    what: PS_BASE_CHECKPOINTS [ck_max][ck_words] u32, PS_BASE_CSTEP [P][3m] u32, PS_BASE_FSTEP [P][m] u32,
    PS_BASE_INFO i32[8], PS_BASE_RESULT i64[2 + 3P], PS_BASE_LAYOUT i32[8] (ck_words, ck_max,

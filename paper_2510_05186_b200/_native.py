@@ -164,6 +164,7 @@ EXPORTS = {
     "ps_base_create": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "ps_base_destroy": (C.c_int, [C.c_void_p]),
     "ps_base_record": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_base_record_explicit": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "ps_base_read": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.POINTER(C.c_size_t)]),
     "ps_bound_batch_eval": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }

@@ -74,6 +74,12 @@ struct ps_base {
     uint32_t *mask;     // [mask_words]
     uint16_t *prev_orders;   // the previously recorded base (a re-recording resumes from its checkpoints)
     uint32_t *prev_mask;
+    // explicit channel orders (ps_base_record_explicit): the base's [G][chan_stride] rows, the
+    // previous base's, and the compute index at which each channel position committed
+    int chan_stride = 0;     // of the current recording (0: derived channel mode)
+    int rec_stride = -1;     // mode of the last recording (-1: none)
+    int cap_stride = 0;
+    uint32_t *chorders = nullptr, *prev_chorders = nullptr, *chstep = nullptr;
 };
 
 namespace {
@@ -310,6 +316,8 @@ void attach_base(const ps_base *B, EvalParams *p) {
     p->base_res = B->res;
     p->base_orders = B->orders;
     p->base_mask = B->mask;
+    p->base_chorders = B->chorders;
+    p->chstep = B->chstep;
     p->ck_interval = B->ck_interval;
     p->ck_words = B->ck_words;
     p->ck_kc = B->K;
@@ -345,7 +353,10 @@ int run_eval(const ps_instance *I, EvalParams p, bool moves, cudaStream_t s, con
     int Ks[3] = {K1, std::min(full, 4 * K1), full};
     int npass = 1;
     if (Ks[0] < full) npass = Ks[1] < full ? 3 : 2;
-    if (B && B->inst == I && p.chorders == nullptr && p.tcode == nullptr) attach_base(B, &p);
+    // a base recorded in the batch's channel mode (explicit: with the same channel-order width)
+    if (B && B->inst == I && p.tcode == nullptr &&
+        (p.chorders == nullptr ? B->chan_stride == 0 : B->chan_stride > 0 && B->chan_stride == p.chan_stride))
+        attach_base(B, &p);
     // worklists, one per handoff between passes: [count][N candidate indices]
     // followed by one dynamic-distribution counter per pass
     int32_t *lists = nullptr;
@@ -856,6 +867,9 @@ int ps_base_destroy(ps_base *B) {
     cudaFree(B->mask);
     cudaFree(B->prev_orders);
     cudaFree(B->prev_mask);
+    cudaFree(B->chorders);
+    cudaFree(B->prev_chorders);
+    cudaFree(B->chstep);
     if (B->info_pending) cudaEventSynchronize(B->info_ev);
     if (B->h_info) cudaFreeHost(B->h_info);
     if (B->info_ev) cudaEventDestroy(B->info_ev);
@@ -863,7 +877,10 @@ int ps_base_destroy(ps_base *B) {
     return PS_OK;
 }
 
-int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, void *stream) {
+static int check_x(const ps_instance *I, const uint32_t *inc_chan, int chan_stride);
+
+static int base_record_impl(ps_base *B, const uint16_t *orders, const uint32_t *mask, const uint32_t *chan,
+                            int32_t chan_stride, void *stream) {
     NvtxRange nvtx("ps_base_record");
     if (!B || !orders || !mask) return fail(PS_ERR_INVALID, "null argument");
     const ps_instance *I = B->inst;
@@ -873,7 +890,28 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     // A usable previous recording is kept: the new base replays it up to their first difference
     // (its checkpoints, cstep and fstep entries before that point are the new base's too).
     refresh_info(B);
-    const bool resume = B->max_window >= 0 && env_int("PS_REC_RESUME", 1) != 0;
+    const bool resume = B->max_window >= 0 && B->rec_stride == chan_stride && env_int("PS_REC_RESUME", 1) != 0;
+    if (chan_stride > 0 && B->cap_stride < chan_stride) {
+        // channel-order tables sized for this width (kept across recordings of the same width)
+        PS_CUDA(cudaStreamSynchronize(s));
+        cudaFree(B->chorders);
+        cudaFree(B->prev_chorders);
+        cudaFree(B->chstep);
+        B->chorders = B->prev_chorders = B->chstep = nullptr;
+        B->cap_stride = 0;
+        const size_t nb = (size_t)I->G * chan_stride * 4;
+        cudaError_t e = cudaMalloc((void **)&B->chorders, nb);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&B->prev_chorders, nb);
+        if (e == cudaSuccess) e = cudaMalloc((void **)&B->chstep, nb);
+        if (e != cudaSuccess) return fail(PS_ERR_NOMEM, "base channel tables: %s", cudaGetErrorString(e));
+        B->cap_stride = chan_stride;
+    }
+    if (resume && chan_stride > 0)
+        PS_CUDA(cudaMemcpyAsync(B->prev_chorders, B->chorders, (size_t)I->G * chan_stride * 4, cudaMemcpyDeviceToDevice, s));
+    if (chan_stride > 0)
+        PS_CUDA(cudaMemcpyAsync(B->chorders, chan, (size_t)I->G * chan_stride * 4, cudaMemcpyDeviceToDevice, s));
+    B->chan_stride = chan_stride;
+    B->rec_stride = chan_stride;
     if (resume) {
         PS_CUDA(cudaMemcpyAsync(B->prev_orders, B->orders, (size_t)I->P * I->stride * 2, cudaMemcpyDeviceToDevice, s));
         PS_CUDA(cudaMemcpyAsync(B->prev_mask, B->mask, (size_t)I->mask_words * 4, cudaMemcpyDeviceToDevice, s));
@@ -883,6 +921,7 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     if (!resume) {
         PS_CUDA(cudaMemsetAsync(B->cstep, 0xFF, (size_t)I->P * I->L * 4, s));
         PS_CUDA(cudaMemsetAsync(B->fstep, 0xFF, (size_t)I->P * I->m * 4, s));
+        if (chan_stride > 0) PS_CUDA(cudaMemsetAsync(B->chstep, 0xFF, (size_t)I->G * chan_stride * 4, s));
     }
     EvalParams p;
     memset(&p, 0, sizeof p);
@@ -894,9 +933,14 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     p.cand_words = B->cand_words;
     p.inc_words = 0;
     attach_base(B, &p);
+    if (chan_stride > 0) {
+        p.chorders = B->chorders;
+        p.chan_stride = chan_stride;
+    }
     if (resume) {
         p.base_orders = B->prev_orders;
         p.base_mask = B->prev_mask;
+        p.base_chorders = B->prev_chorders;
         p.rec_prev = 1;
     }
     LaunchCfg cfg;
@@ -927,6 +971,18 @@ int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, voi
     PS_CUDA(cudaEventRecord(B->info_ev, s));
     B->info_pending = true;
     return PS_OK;
+}
+
+int ps_base_record(ps_base *B, const uint16_t *orders, const uint32_t *mask, void *stream) {
+    return base_record_impl(B, orders, mask, nullptr, 0, stream);
+}
+
+int ps_base_record_explicit(ps_base *B, const uint16_t *orders, const uint32_t *mask, const uint32_t *chan_orders,
+                            int32_t chan_stride, void *stream) {
+    if (!B || !chan_orders || chan_stride < 1) return fail(PS_ERR_INVALID, "channel orders and a positive width are required");
+    int rc = check_x(B->inst, chan_orders, chan_stride);
+    if (rc) return rc;
+    return base_record_impl(B, orders, mask, chan_orders, chan_stride, stream);
 }
 
 int ps_base_read(const ps_base *B, int what, void *host, size_t *bytes) {
@@ -1683,7 +1739,7 @@ int ps_search_round_explicit(const ps_instance *I, const ps_search_desc *d, cons
         p.bubble = bub;
         p.flags = flg;
         p.events_total = (unsigned long long *)d->events_total;
-        rc = run_eval(I, p, false, s, nullptr);
+        rc = run_eval(I, p, false, s, d->base);   // (prefix sharing with an explicit recording of the incumbent)
         if (rc) return rc;
         best_key_kernel<<<std::max(1, std::min((int)((n + 255) / 256), 4 * I->num_sms)), 256, 0, s>>>(
             p.makespan, flg, n, d->first_index + lo, (long long *)best_key);

@@ -107,6 +107,9 @@ struct EvalParams {
                              // times [2+2P, 2+3P) first starts
     const uint16_t *base_orders;   // [P][stride] (materialised candidates; REC: the previous base)
     const uint32_t *base_mask;     // [mask_words]
+    const uint32_t *base_chorders; // [G][chan_stride] explicit-channel base (REC: the previous base's)
+    uint32_t *chstep;              // [G][chan_stride] compute events committed when the base commits
+                                   // the transfer at that position of its channel order (~0 = never)
     int rec_prev;                  // REC: resume from the previous base's checkpoints
 };
 
@@ -404,6 +407,7 @@ eval_kernel(const EvalParams p) {
     uint32_t chead = NO_CHAN, cnext = NO_CHAN;
     int wt = -1;        // see compute_key
     int lastq = -1;     // last position of this stage's order that differs from the base's
+    int lastqc = -1;    // explicit channels: last position of this lane's channel order that differs
     int eoff = 0;       // base step = candidate step + eoff once the candidate's extra/missing transfers are done
     // Row bands.  A stage's end-time rows are A_DEAD (A row) / zero (X row) below the
     // band of microbatches in flight and zero above it, in the slot as in every checkpoint (whose band
@@ -690,6 +694,7 @@ eval_kernel(const EvalParams p) {
     auto save_regs = [&](uint32_t *rg) {
         rg[0] = pos; rg[1] = sfree; rg[2] = cfree; rg[3] = ws; rg[4] = we; rg[5] = n_poff; rg[6] = n_prel;
         rg[7] = n_unrel; rg[8] = first_start;
+        rg[23] = (uint32_t)cpos;                 // explicit channels: this lane's channel cursor
         *reinterpret_cast<long long *>(rg + 12) = (long long)base;
         *reinterpret_cast<long long *>(rg + 14) = (long long)top;
         *reinterpret_cast<long long *>(rg + 16) = (long long)peak;
@@ -697,6 +702,7 @@ eval_kernel(const EvalParams p) {
     auto load_regs = [&](const uint32_t *rg) {
         pos = rg[0]; sfree = rg[1]; cfree = rg[2]; ws = rg[3]; we = rg[4]; n_poff = rg[5]; n_prel = rg[6];
         n_unrel = rg[7]; first_start = rg[8];
+        if (!derived) cpos = (int)rg[23];
         base = (V)*reinterpret_cast<const long long *>(rg + 12);
         top = (V)*reinterpret_cast<const long long *>(rg + 14);
         peak = (V)*reinterpret_cast<const long long *>(rg + 16);
@@ -832,7 +838,7 @@ eval_kernel(const EvalParams p) {
             // a channel that has carried nothing yet (free time 0 on both) constrains nothing
             // (nor does an own channel with nothing in flight that is already behind the stage: every
             // later transfer on it waits for an F not committed yet)
-            eq = pos == (int)rg[0] && sfree - (int)rg[1] == d &&
+            eq = pos == (int)rg[0] && sfree - (int)rg[1] == d && (derived || cpos == (int)rg[23]) &&
                  (cfree - (int)rg[2] == d || (cfree == 0 && rg[2] == 0u) ||
                   (derived && chan_excl && n_poff == 0 && n_prel == 0 && cfree <= sfree && rg[2] <= rg[1])) &&
                  we - ws == (int)rg[4] &&
@@ -1091,6 +1097,7 @@ eval_kernel(const EvalParams p) {
         };
         int cand_unrel = 0;
         lastq = -1;
+        lastqc = -1;
         int dq = L;         // first position where the row differs from the recorded base's
         if (has_stage) {
             cand_unrel = build_mask(true);
@@ -1200,6 +1207,30 @@ eval_kernel(const EvalParams p) {
                     }
                 }
                 eoff = nbase - cand_unrel;
+            }
+            if (!derived) {
+                // explicit channel orders: lane g compares channel g's order with the base's; the
+                // first difference at position q takes effect once the base has committed the
+                // transfer at q - 1 (checkpoints before the compute event preceding it are safe)
+                int lq = -1;
+                if (lane < p.G) {
+                    const uint32_t *crow = p.chorders + ((size_t)cand * p.G + lane) * p.chan_stride;
+                    const uint32_t *brow = p.base_chorders + (size_t)lane * p.chan_stride;
+                    int qc = 0;
+                    while (qc < p.chan_stride && crow[qc] == brow[qc]) ++qc;
+                    if (qc < p.chan_stride) {
+                        int e = p.chan_stride - 1;
+                        while (e > qc && crow[e] == brow[e]) --e;
+                        lq = e;
+                        uint32_t dc = 0u;
+                        if (qc > 0) {
+                            const uint32_t y = p.chstep[(size_t)lane * p.chan_stride + qc - 1];
+                            dc = y == NEVER ? NEVER : (y > 0u ? y - 1u : 0u);
+                        }
+                        d = min(d, dc);
+                    }
+                }
+                lastqc = __shfl_sync(0xffffffffu, lq, chan_i >= 0 ? chan_i : 0);
             }
             // the base runs two transfer events per offloaded activation the candidate does not have
             eoff = 2 * __reduce_add_sync(0xffffffffu, eoff);
@@ -1341,7 +1372,8 @@ eval_kernel(const EvalParams p) {
         ovf = false;
         rF = rG = NO_R;
         head = fetch(pos); nxt = fetch(pos + 1);
-        cpos = 0; chead = fetch_chan(0); cnext = fetch_chan(1);
+        if (ck_idx <= 0) cpos = 0;                   // (a restored candidate resumes its channel cursor)
+        chead = fetch_chan(cpos); cnext = fetch_chan(cpos + 1);
         cdirty = tdirty = has_stage;
         ckey = tkey = KEY_ABSENT;
         __syncwarp();
@@ -1398,7 +1430,7 @@ eval_kernel(const EvalParams p) {
                 // base's shifted (rec_shift_kernel).
                 if (REC) canon_dominated();
                 if ((REC ? n_src > 1 : n_ck > 1) && cc > (int)div && c < n_src) {
-                    const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead()));
+                    const bool gate = !ovf && (!has_stage || (pos > lastq && diff_dead() && (derived || cpos > lastqc)));
                     if (__all_sync(0xffffffffu, gate)) {
                         if (same_state(c)) {
                             conv_c = c;
@@ -1543,6 +1575,7 @@ eval_kernel(const EvalParams p) {
                     cfree = end;
                     tdirty = true;
                     if (!derived) {
+                        if (REC && i == w) p.chstep[(size_t)chan_i * p.chan_stride + cpos] = (uint32_t)cc;
                         ++cpos;
                         chead = cnext;
                         cnext = fetch_chan(cpos + 1);
@@ -1656,6 +1689,8 @@ eval_kernel(const EvalParams p) {
                 // deadlocked base: what it never committed is NEVER (a resumed recording would
                 // otherwise keep the previous base's steps there)
                 for (int q = pos; q < L; ++q) p.cstep[i * L + q] = NEVER;
+                if (!derived)      // (every lane of a channel writes the same entries)
+                    for (int q = cpos; q < p.chan_stride; ++q) p.chstep[(size_t)chan_i * p.chan_stride + q] = NEVER;
                 for (int j = 0; j < m; ++j)
                     if ((SW(o_Ai + (j)) & 3u) == 0u) p.fstep[i * m + j] = NEVER;
             }

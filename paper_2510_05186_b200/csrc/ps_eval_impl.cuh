@@ -48,8 +48,10 @@ static cudaError_t occ_one(int block, size_t smem, int *n) {
 // Move-encoded candidates (the search) are always in derived channel mode; base recording is a
 // single materialised candidate in derived mode with its state in shared memory.
 #define PS_PICK(FN, ARGS)                                                                              \
-    if (!MOVES && v.record)                                                                           \
+    if (!MOVES && v.record && v.derived)                                                              \
         return v.uni ? FN<V, false, 0, true, true, true> ARGS : FN<V, false, 0, true, true, false> ARGS; \
+    if (!MOVES && v.record)                                                                           \
+        return v.uni ? FN<V, false, 0, true, false, true> ARGS : FN<V, false, 0, true, false, false> ARGS; \
     if (MOVES || v.derived) {                                                                         \
         if (v.gstate && v.wmask) return v.uni ? FN<V, MOVES, 2, false, true, true> ARGS : FN<V, MOVES, 2, false, true, false> ARGS; \
         if (v.gstate) return v.uni ? FN<V, MOVES, 1, false, true, true> ARGS : FN<V, MOVES, 1, false, true, false> ARGS; \

@@ -209,6 +209,12 @@ class Base:
         N.check(self.di.lib.ps_base_record(self.handle, C.c_void_p(orders.data_ptr()),
                                            C.c_void_p(mask.data_ptr()), self.di._stream(stream)))
 
+    def record_explicit(self, orders, mask, chans, stream=None):
+        """With explicit channel orders: chans device int32 [G, width] (ps_base_record_explicit)."""
+        N.check(self.di.lib.ps_base_record_explicit(self.handle, C.c_void_p(orders.data_ptr()),
+                                                    C.c_void_p(mask.data_ptr()), C.c_void_p(chans.data_ptr()),
+                                                    int(chans.shape[-1]), self.di._stream(stream)))
+
     def read(self, what: int):
         """One recorded table (N.BASE_*) as raw bytes (synchronises the device)."""
         n = C.c_size_t(0)

@@ -409,6 +409,12 @@ class ChannelSearch:
         self.round = 0
         self.evaluated = 0
         self.improvements = []
+        # the incumbent recorded with its channel orders: neighbours resume from its checkpoints
+        self.base = None
+        if config.share_prefix:
+            from .engine import Base
+            self.base = Base(self.di)
+            self.base.record_explicit(self.inc_orders, self.inc_mask, self.inc_chan)
 
     @classmethod
     def from_schedule(cls, inst, schedule, config: SearchConfig = SearchConfig(), device=None):
@@ -425,7 +431,7 @@ class ChannelSearch:
         count = self.cfg.neighbours if count is None else count
         self.best_key.fill_(N.BEST_NONE)
         desc = N.SearchDesc(self.inc_orders.data_ptr(), self.inc_mask.data_ptr(), self.round, first, count,
-                            self.moves, None, None, 0)
+                            self.moves, None, self.base.handle if self.base is not None else None, 0)
         N.check(self.lib.ps_search_round_explicit(
             self.di.handle, C.byref(desc), C.c_void_p(self.inc_chan.data_ptr()), self.chan_stride,
             C.c_void_p(self.best_key.data_ptr()),
@@ -443,6 +449,8 @@ class ChannelSearch:
         N.check(self.lib.ps_apply_move_explicit(self.di.handle, C.c_void_p(self.inc_orders.data_ptr()),
                                                 C.c_void_p(self.inc_chan.data_ptr()), self.chan_stride,
                                                 C.byref(self.moves), r, idx, self._stream()))
+        if self.base is not None:
+            self.base.record_explicit(self.inc_orders, self.inc_mask, self.inc_chan)
         self.makespan = span
         self.improvements.append(Improvement(r, span, (time.perf_counter() - t0) if t0 else 0.0, idx))
         return True

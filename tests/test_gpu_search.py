@@ -493,6 +493,37 @@ def test_channel_search_rounds_and_trail_match_the_cpu_restatement(cuda_ok):
     assert validate(res.schedule, inst).ok and makespan(res.schedule, inst) == span
 
 
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_channel_search_prefix_sharing_is_exact(cuda_ok, cfg):
+    """Channel-order search with the incumbent recorded in explicit channel mode (checkpoints with
+    channel cursors, per-position commit steps) against the same search with every
+    neighbour simulated in full: equal makespans for every neighbour of every round, the same
+    adopted moves, the same final channel orders — across re-recordings of the incumbent."""
+    import torch
+    from paper_2510_05186_b200 import workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.search import ChannelSearch, SearchConfig
+    inst = workloads.CONFIGS[cfg]()
+    s, _ = best_feasible(inst)
+    n = 8192 if cfg != 4 else 2048
+    runs = []
+    for share in (True, False):
+        cs = ChannelSearch.from_schedule(inst, s, SearchConfig(seed=SEED, neighbours=n, shift_permille=400,
+                                                               max_shift=MAXSHIFT, share_prefix=share))
+        spans = []
+        for _ in range(8):
+            ms = torch.empty(n, dtype=torch.int64, device="cuda")
+            cs.launch_round(ms)
+            spans.append(ms.cpu().numpy())
+            cs.step()            # (runs the round again, then adopts its winner and re-records)
+        runs.append((spans, [(i.round, i.makespan) for i in cs.improvements], cs.inc_chan.cpu().numpy().copy()))
+    (a, ta, ca), (b, tb, cb) = runs
+    for r, (x, y) in enumerate(zip(a, b)):
+        assert (x == y).all(), (cfg, r, int((x != y).sum()))
+    assert ta == tb and len(ta) >= 1
+    assert (ca == cb).all()
+
+
 @pytest.mark.parametrize("late", [False, True])
 def test_bound_pruning_keeps_every_round_decision(cuda_ok, late):
     """Search rounds with the incumbent's makespan as cutoff abandon neighbours
