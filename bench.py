@@ -398,14 +398,19 @@ def main():
     achieved = ops_per_launch / kern_s / 1e12
     # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from the committed ncu --set full
     # capture of the same command (ncu cannot run inside the timed bench)
-    traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", {3: "ncu_eval_summary.json", 5: "ncu_eval_config5_summary.json"}.get(
-        CONFIG, "ncu_eval_config%d_summary.json" % CONFIG))
+    traffic, traffic_src, hw = None, None, None
+    prof_name = {3: "ncu_eval_summary.json", 5: "ncu_eval_config5_summary.json"}.get(
+        CONFIG, "ncu_eval_config%d_summary.json" % CONFIG)
+    prof = os.path.join(ROOT, "profiles", prof_name)
     if os.path.exists(prof):
         try:
             doc = json.load(open(prof))
             traffic = doc.get("dram_bytes_per_launch")
-            traffic_src = f"profiles/ncu_eval_summary.json (round {doc.get('round')}, {doc.get('kernel')})"
+            traffic_src = f"profiles/{prof_name} (round {doc.get('round')}, {doc.get('kernel')})"
+            # what the hardware was doing in that capture: the kernel is issue-bound, not idle
+            hw = {k: doc.get(k) for k in ("issue_active_pct", "alu_pipe_pct", "warps_active_pct",
+                                          "threads_per_warp_instruction", "warp_instructions", "duration_ms")}
+            hw["source"] = traffic_src
         except Exception:
             traffic = None
     n_cand = cfg.neighbours // world
@@ -420,6 +425,7 @@ def main():
         "frac": achieved / int32_peak, "traffic": traffic, "traffic_source": traffic_src,
         "kernel": "ps::eval_kernel<int, moves, smem state, derived channels, symmetric tables> (search round)",
         "kernel_ms_per_launch": 1000 * kern_s, "kernel_share_of_step": sum(kern_ms) / sum(step_ms),
+        "ncu_utilisation": hw,
         "algorithmic_events_per_launch": ev_full / K, "simulated_events_per_launch": ev_sim / K,
         "int_ops_per_event": 10,
         "peak_source": "ps_int32_probe measured live on this GPU (IADD3/LOP3/IMAD chains)",
