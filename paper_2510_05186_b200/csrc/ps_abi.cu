@@ -334,7 +334,13 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
 // round needs it, it has long landed).
 void refresh_info(const ps_base *B) {
     if (!B->info_pending) return;
-    cudaEventSynchronize(B->info_ev);
+    // Not landed yet (the recording is still running): keep the last known values instead of
+    // stalling the host — they only size the first pass's ledger window and hint whether a
+    // re-recording may resume; the kernels read the recording's own info from device memory, and
+    // a window that turns out too small is caught by the overflow passes, so results never
+    // depend on it.
+    if (env_int("PS_INFO_WAIT", 0) != 0) cudaEventSynchronize(B->info_ev);
+    else if (cudaEventQuery(B->info_ev) != cudaSuccess) return;
     B->max_window = B->h_info[0] > 0 ? B->h_info[4] : -1;
     B->info_pending = false;
 }
