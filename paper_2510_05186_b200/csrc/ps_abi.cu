@@ -543,7 +543,10 @@ __global__ void divergence_kernel(MoveCtx c, ps_move_params mp, uint64_t round, 
     } else if (mv.type == MOVE_TOGGLE) {
         d = fstep[mv.stage * c.m + mv.mb];
     }
-    key[n] = d;
+    // (no-ops and never-reached steps sort last: keys stay below 3Pm + 1, so the radix sort only
+    // needs the bits of 3Pm)
+    const uint32_t last = (uint32_t)(c.P * c.L);
+    key[n] = d < last ? d : last;
     idx[n] = (int32_t)n;
 }
 
@@ -617,7 +620,9 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
     int32_t *idx = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
-    PS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, 32, s));
+    int key_bits = 1;
+    while (key_bits < 32 && ((int64_t)I->P * I->L) >> key_bits) ++key_bits;
+    PS_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, key_bits, s));
     PS_CUDA(cudaMallocAsync((void **)&keys, (size_t)N * 4, s));
     PS_CUDA(cudaMallocAsync((void **)&keys_out, (size_t)N * 4, s));
     PS_CUDA(cudaMallocAsync((void **)&idx, (size_t)N * 4, s));
@@ -625,7 +630,7 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
     divergence_kernel<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N,
                                                                  p.cstep, p.fstep, keys, idx, order, p.move_list);
     PS_CUDA(cudaGetLastError());
-    PS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, 32, s));
+    PS_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_out, idx, order + 1, (int)N, 0, key_bits, s));
     cudaFreeAsync(keys, s);
     cudaFreeAsync(keys_out, s);
     cudaFreeAsync(idx, s);
