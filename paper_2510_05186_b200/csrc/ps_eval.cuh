@@ -1166,6 +1166,20 @@ eval_kernel(const EvalParams p) {
                 }
             }
         }
+        if (!MOVES && !derived && lane < p.G) {
+            // explicit channel orders name offloaded activations of stages on their channel (the
+            // literal replay decides what the reference does with anything else)
+            const uint32_t *crow = p.chorders + ((size_t)cand * p.G + lane) * p.chan_stride;
+            const int mwords = (P * m + 31) / 32;
+            for (int q = 0; q < p.chan_stride && !bad; ++q) {
+                const uint32_t e = __ldg(crow + q);
+                if (e == NO_CHAN) break;
+                const int s2 = (int)((e >> 16) & 0x7FFFu), j2 = (int)(e & 0xFFFFu);
+                if (s2 >= P || j2 >= m || __ldg(&p.chan[s2]) != lane) { bad = true; break; }
+                const int bit = s2 * m + j2;
+                if (!((__ldcg(&p.masks[(size_t)cand * mwords + (bit >> 5)]) >> (bit & 31)) & 1u)) bad = true;
+            }
+        }
         if (__any_sync(0xffffffffu, bad)) {
             if (lane == 0) put_result(FLAG_MALFORMED, -1LL, 0u, 0);
             if (REC && lane == 0) {

@@ -288,3 +288,42 @@ def test_delta_batch_moves_and_general_candidates(cuda_ok, cfg):
     bad[int(doff[3]), 0] = (pk.num_stages << 16)           # stage out of range
     with pytest.raises(N.NativeError):
         di.evaluate_host_delta(ref_o, ref_m, doff, bad, foff, flips, peak=True, base=ls.base)
+
+
+def test_explicit_channel_entries_out_of_range_are_malformed(cuda_ok):
+    """Explicit channel orders through the C ABI with entries that name a microbatch past m, a
+    stage on another channel or an activation that is not offloaded: the candidate is
+    PS_FLAG_MALFORMED (no out-of-range state access), its neighbours in the batch are unaffected."""
+    import torch
+    from paper_2510_05186_b200 import _native as N, workloads
+    from paper_2510_05186_b200.heuristics import best_feasible
+    from paper_2510_05186_b200.search import ChannelSearch, SearchConfig
+    for cfg in (2, 4):
+        inst = workloads.CONFIGS[cfg]()
+        s, _ = best_feasible(inst)
+        cs = ChannelSearch.from_schedule(inst, s, SearchConfig(seed=1, neighbours=64, share_prefix=False))
+        o, mk, ch = cs.materialize(0, 8, 0)
+        ch = ch.clone()
+        m = inst.num_microbatches
+        e = int(ch[1, 0, 0].item()) & 0xFFFFFFFF
+        ch[1, 0, 0] = torch.tensor(((e & ~0xFFFF) | (m + 3)) - (1 << 32) if (e & ~0xFFFF) | (m + 3) >= 1 << 31
+                                   else (e & ~0xFFFF) | (m + 3), dtype=torch.int32)          # microbatch past m
+        other = 1 if cs.di.packed.num_channels > 1 else 0
+        e2 = int(ch[2, other, 0].item()) & 0xFFFFFFFF
+        ch[2, 0, 0] = torch.tensor(e2 - (1 << 32) if e2 >= 1 << 31 else e2, dtype=torch.int32)  # stage of another channel
+        mk = mk.clone()
+        st, j = (e >> 16) & 0x7FFF, e & 0xFFFF
+        b = st * m + j
+        mk[3, b >> 5] ^= torch.tensor((1 << (b & 31)) - (1 << 32) if (b & 31) == 31 else 1 << (b & 31),
+                                      dtype=torch.int32)                                     # not offloaded
+        r = cs.di.evaluate(o, mk, ch, peak=False)
+        torch.cuda.synchronize()
+        flags = r.flags.cpu().numpy()
+        assert flags[1] == N.FLAG_MALFORMED and flags[3] == N.FLAG_MALFORMED, (cfg, flags)
+        if other:
+            assert flags[2] == N.FLAG_MALFORMED, (cfg, flags)
+        good = [0] + list(range(4, 8))
+        r0 = cs.di.evaluate(o[good], mk[good], ch[good], peak=False)
+        torch.cuda.synchronize()
+        assert (r0.flags.cpu().numpy() == flags[good]).all()
+        assert (r0.makespan.cpu().numpy() == r.makespan.cpu().numpy()[good]).all()
