@@ -152,7 +152,9 @@ typedef struct ps_move_params {
 } ps_move_params;
 
 typedef struct ps_search_desc {
-    const uint16_t *inc_orders;     /* device [P][order_stride]: incumbent structure              */
+    const uint16_t *inc_orders;     /* device [P][order_stride]: incumbent structure — each stage
+                                       row a permutation of its 3m ops (not re-validated per round;
+                                       ps_eval_batch validates a structure, ps_apply_move keeps one) */
     const uint32_t *inc_mask;       /* device [mask_words]                                         */
     uint64_t round;
     int64_t first_index;            /* global index of this shard's first neighbour               */
