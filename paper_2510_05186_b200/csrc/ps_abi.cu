@@ -552,12 +552,20 @@ __global__ void divergence_kernel(MoveCtx c, ps_move_params mp, uint64_t round, 
 
 // Distinct moves of a round, in LPT order: key = divergence:15 | shift:1 | stage:5 | a:13 | b:13 |
 // index:17 (an adjacent shift a->a+1 is the same permutation as a+1->a; a no-op has a = b = 8191).
+// Dedup keys, packed as tightly as the instance allows (fewer radix passes):
+// divergence (db bits, never-reached capped at 3Pm) | shift? | stage (sb) | a (ab) | b (ab) | index (17).
+struct DedupLayout {
+    int db, sb, ab;
+};
+
 __global__ void dedup_key_kernel(MoveCtx c, ps_move_params mp, uint64_t round, int64_t first, int64_t count,
-                                 const uint32_t *cstep, const uint32_t *fstep, unsigned long long *key) {
+                                 const uint32_t *cstep, const uint32_t *fstep, DedupLayout lay,
+                                 unsigned long long *key) {
     const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= count) return;
     const Move mv = ctx_decode(c, mp, round, (uint64_t)(first + n));
-    uint32_t d = 0x7FFFu, sh = 0, st = 0, a = 8191, bb = 8191;
+    const uint32_t dmax = (uint32_t)(c.P * c.L), none = (1u << lay.ab) - 1u;
+    uint32_t d = dmax, sh = 0, st = 0, a = none, bb = none;
     if (mv.type == MOVE_SHIFT) {
         const int q = mv.a < mv.b ? mv.a : mv.b;
         d = q == 0 ? 0u : cstep[mv.stage * c.L + q - 1];
@@ -567,9 +575,10 @@ __global__ void dedup_key_kernel(MoveCtx c, ps_move_params mp, uint64_t round, i
         d = fstep[mv.stage * c.m + mv.mb];
         st = mv.stage; a = mv.mb; bb = 0;
     }
-    if (d > 0x7FFFu) d = 0x7FFFu;
-    key[n] = ((unsigned long long)d << 49) | ((unsigned long long)sh << 48) | ((unsigned long long)st << 43) |
-             ((unsigned long long)a << 30) | ((unsigned long long)bb << 17) | (unsigned long long)n;
+    if (d > dmax) d = dmax;
+    const int pb = 17, pa = pb + lay.ab, ps = pa + lay.ab, psh = ps + lay.sb, pd = psh + 1;
+    key[n] = ((unsigned long long)d << pd) | ((unsigned long long)sh << psh) | ((unsigned long long)st << ps) |
+             ((unsigned long long)a << pa) | ((unsigned long long)bb << pb) | (unsigned long long)n;
 }
 
 __global__ void dedup_head_kernel(const unsigned long long *sorted, int64_t count, int32_t *idx, unsigned char *head) {
@@ -585,7 +594,13 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
     mp.seed = p.seed;
     mp.shift_permille = p.shift_permille;
     mp.max_shift = p.max_shift;
-    if (p.dedup && N <= (1 << 17) && 3 * I->m < 8191 && 3 * I->P * I->m < 0x7FFF) {
+    auto bits_of = [](int64_t v) { int b = 1; while (b < 63 && (v >> b)) ++b; return b; };
+    DedupLayout lay;
+    lay.db = bits_of((int64_t)I->P * I->L);
+    lay.sb = bits_of(I->P - 1);
+    lay.ab = bits_of(I->L);
+    const int key_bits64 = lay.db + 1 + lay.sb + 2 * lay.ab + 17;
+    if (p.dedup && N <= (1 << 17) && key_bits64 <= 64) {
         // the same move drawn several times in a round is simulated once: its lowest index
         // carries it, so the round's best key is unchanged
         unsigned long long *keys = nullptr, *sorted = nullptr;
@@ -593,7 +608,7 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
         unsigned char *head = nullptr;
         void *tmp = nullptr;
         size_t b1 = 0, b2 = 0;
-        PS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, keys, sorted, (int)N, 0, 64, s));
+        PS_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, keys, sorted, (int)N, 0, key_bits64, s));
         PS_CUDA(cub::DeviceSelect::Flagged(nullptr, b2, idx, head, order + 1, order, (int)N, s));
         PS_CUDA(cudaMallocAsync((void **)&keys, (size_t)N * 8, s));
         PS_CUDA(cudaMallocAsync((void **)&sorted, (size_t)N * 8, s));
@@ -601,10 +616,10 @@ int order_by_divergence(const ps_instance *I, const EvalParams &p, int32_t *orde
         PS_CUDA(cudaMallocAsync((void **)&head, (size_t)N, s));
         PS_CUDA(cudaMallocAsync(&tmp, std::max(b1, b2), s));
         const unsigned g = (unsigned)((N + 255) / 256);
-        dedup_key_kernel<<<g, 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N, p.cstep, p.fstep, keys);
+        dedup_key_kernel<<<g, 256, 0, s>>>(move_ctx(I), mp, p.round, p.first_index, N, p.cstep, p.fstep, lay, keys);
         PS_CUDA(cudaGetLastError());
         size_t tb = std::max(b1, b2);
-        PS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)N, 0, 64, s));
+        PS_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tb, keys, sorted, (int)N, 0, key_bits64, s));
         dedup_head_kernel<<<g, 256, 0, s>>>(sorted, N, idx, head);
         PS_CUDA(cudaGetLastError());
         tb = std::max(b1, b2);
