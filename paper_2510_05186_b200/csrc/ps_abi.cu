@@ -181,9 +181,14 @@ bool wmask_shape(int MW) {
 
 // Materialised shared-memory passes with no recorded base run the full-simulation build (no
 // checkpoint code, 7 blocks per SM): no-base batches 55.4 -> 49.7 ms at config 3 (r02 A/B).
-bool nobase_build(bool moves, bool gstate, bool record, bool has_base) {
+// With global state (GS 4, one-warp blocks at 80 registers, up to 24 per SM) it pays only for
+// states of up to ~40 KB: config 4 (33 KB with its staged rows) 445 -> 342 ms per 65,536 full
+// simulations; config 5 (118 KB) was slower at 16 or 24 blocks per SM (1.23-1.39 vs 1.13 s) and
+// keeps the general build.
+bool nobase_build(bool moves, bool gstate, bool record, bool has_base, int cand_words = 0) {
     static const int on = env_int("PS_NOBASE_BUILD", 1);
-    return on && !moves && !gstate && !record && !has_base;
+    if (gstate && (int64_t)cand_words * 4 > env_int("PS_GNB_MAX_BYTES", 40960)) return false;
+    return on && !moves && !record && !has_base;
 }
 
 cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, LaunchCfg c, cudaStream_t s,
@@ -194,7 +199,7 @@ cudaError_t launch(bool v64, bool moves, bool gstate, const EvalParams &p, Launc
     v.derived = p.chorders == nullptr;
     v.uni = p.uniform != 0;
     v.wmask = gstate && wmask_shape(p.MW);
-    v.nobase = nobase_build(moves, gstate, record, p.ck != nullptr);
+    v.nobase = nobase_build(moves, gstate, record, p.ck != nullptr, p.cand_words);
     if (v64) return moves ? eval_launch<long long, true>(v, p, c, s) : eval_launch<long long, false>(v, p, c, s);
     return moves ? eval_launch<int, true>(v, p, c, s) : eval_launch<int, false>(v, p, c, s);
 }
@@ -243,7 +248,7 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         v.derived = true;
         v.uni = I->uniform != 0;
         v.wmask = pl->gstate && wmask_shape(I->MW);
-        v.nobase = nobase_build(moves, pl->gstate, false, has_base);
+        v.nobase = nobase_build(moves, pl->gstate, false, has_base, pl->cand_words);
         const uint64_t okey = ((uint64_t)pl->cfg.smem << 16) | ((uint64_t)pl->cfg.block << 3) |
                               ((uint64_t)v.nobase << 2) | ((uint64_t)pl->gstate << 1) | (uint64_t)moves;
         *per_sm = 0;
@@ -294,8 +299,10 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         return fail(PS_ERR_RANGE, "incumbent does not fit in shared memory");
     if (pl->gstate && (rc = blocks_per_sm(&per_sm)) != PS_OK) return rc;
     int64_t want = (N + pl->warps - 1) / pl->warps;
-    int64_t cap = pl->gstate ? std::min<int64_t>(per_sm, env_int("PS_GSTATE_BLOCKS_PER_SM", 16)) * I->num_sms
-                             : (int64_t)per_sm * I->num_sms;
+    // global state: at most 16 blocks per SM, except the no-base build's one-warp blocks
+    const bool gnb = pl->gstate && nobase_build(moves, true, false, has_base, pl->cand_words);
+    int64_t cap = pl->gstate && !gnb ? std::min<int64_t>(per_sm, env_int("PS_GSTATE_BLOCKS_PER_SM", 16)) * I->num_sms
+                                     : (int64_t)per_sm * I->num_sms;
     pl->cfg.grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, cap));
     pl->scratch_bytes = pl->gstate ? (size_t)pl->cfg.grid * pl->warps * pl->cand_words * 4 : 0;
     return PS_OK;

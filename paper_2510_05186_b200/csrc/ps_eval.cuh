@@ -271,6 +271,9 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 #ifndef PS_MIN_BLOCKS_G
 #define PS_MIN_BLOCKS_G 1     // global-memory state: one 16-warp block per SM, 122 registers (r01 A/B)
 #endif
+#ifndef PS_MIN_BLOCKS_GNB
+#define PS_MIN_BLOCKS_GNB 24  // global state without a base: one-warp blocks, <= 85 registers
+#endif
 #ifndef PS_MIN_BLOCKS_NB
 #define PS_MIN_BLOCKS_NB 7    // materialised candidates without a base: full simulations (r02 A/B: 7 is -10% vs 5)
 #endif
@@ -288,14 +291,15 @@ constexpr unsigned long long KEY_ABSENT = ~0ull;
 // GS: per-candidate state in shared memory (0), in global scratch (1), in global scratch with
 // nonzero-word masks over the pending-transfer sets (2: many bitset words per stage, config 5),
 // in shared memory without a recorded base (3: materialised full simulations; no checkpoint code,
-// built for 7 blocks per SM like the move-encoded kernel).
+// built for 7 blocks per SM like the move-encoded kernel), in global scratch without a base (4:
+// materialised full simulations of large shapes, one-warp blocks, PS_MIN_BLOCKS_GNB per SM).
 template <typename V, bool MOVES, int GS, bool REC, bool DERIVED, bool UNI>
-__global__ void __launch_bounds__((GS == 1 || GS == 2) ? 32 * PS_GSTATE_MAX_WARPS : 128,
-                                  REC ? 1 : (GS == 1 || GS == 2) ? PS_MIN_BLOCKS_G
+__global__ void __launch_bounds__((GS == 1 || GS == 2) ? 32 * PS_GSTATE_MAX_WARPS : GS == 4 ? 32 : 128,
+                                  REC ? 1 : (GS == 1 || GS == 2) ? PS_MIN_BLOCKS_G : GS == 4 ? PS_MIN_BLOCKS_GNB
                                   : GS == 3 ? PS_MIN_BLOCKS_NB : (MOVES ? PS_MIN_BLOCKS : PS_MIN_BLOCKS_MAT))
 eval_kernel(const EvalParams p) {
-    constexpr bool GSTATE = GS == 1 || GS == 2;
-    constexpr bool NOBASE = GS == 3;
+    constexpr bool GSTATE = GS == 1 || GS == 2 || GS == 4;
+    constexpr bool NOBASE = GS == 3 || GS == 4;
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int VW = sizeof(V) / 4;
     const int lane = threadIdx.x & 31;

@@ -53,22 +53,26 @@ static cudaError_t occ_one(int block, size_t smem, int *n) {
     if (!MOVES && v.record)                                                                           \
         return v.uni ? FN<V, false, 0, true, false, true> ARGS : FN<V, false, 0, true, false, false> ARGS; \
     if (MOVES || v.derived) {                                                                         \
+        if (!MOVES && v.gstate && v.nobase) return v.uni ? FN<V, MOVES, 4, false, true, true> ARGS : FN<V, MOVES, 4, false, true, false> ARGS; \
         if (v.gstate && v.wmask) return v.uni ? FN<V, MOVES, 2, false, true, true> ARGS : FN<V, MOVES, 2, false, true, false> ARGS; \
         if (v.gstate) return v.uni ? FN<V, MOVES, 1, false, true, true> ARGS : FN<V, MOVES, 1, false, true, false> ARGS; \
         if (!MOVES && v.nobase) return v.uni ? FN<V, MOVES, 3, false, true, true> ARGS : FN<V, MOVES, 3, false, true, false> ARGS; \
         return v.uni ? FN<V, MOVES, 0, false, true, true> ARGS : FN<V, MOVES, 0, false, true, false> ARGS; \
     }                                                                                                 \
+    if (v.gstate && v.nobase) return v.uni ? FN<V, false, 4, false, false, true> ARGS : FN<V, false, 4, false, false, false> ARGS; \
     if (v.gstate) return v.uni ? FN<V, false, 1, false, false, true> ARGS : FN<V, false, 1, false, false, false> ARGS; \
     if (v.nobase) return v.uni ? FN<V, false, 3, false, false, true> ARGS : FN<V, false, 3, false, false, false> ARGS; \
     return v.uni ? FN<V, false, 0, false, false, true> ARGS : FN<V, false, 0, false, false, false> ARGS;
 
 #define PS_PICK_OCC(FN, ARGS)                                                                          \
     if (MOVES || v.derived) {                                                                         \
+        if (!MOVES && v.gstate && v.nobase) return v.uni ? FN<V, MOVES, 4, true, true> ARGS : FN<V, MOVES, 4, true, false> ARGS; \
         if (v.gstate && v.wmask) return v.uni ? FN<V, MOVES, 2, true, true> ARGS : FN<V, MOVES, 2, true, false> ARGS; \
         if (v.gstate) return v.uni ? FN<V, MOVES, 1, true, true> ARGS : FN<V, MOVES, 1, true, false> ARGS; \
         if (!MOVES && v.nobase) return v.uni ? FN<V, MOVES, 3, true, true> ARGS : FN<V, MOVES, 3, true, false> ARGS; \
         return v.uni ? FN<V, MOVES, 0, true, true> ARGS : FN<V, MOVES, 0, true, false> ARGS; \
     }                                                                                                 \
+    if (v.gstate && v.nobase) return v.uni ? FN<V, false, 4, false, true> ARGS : FN<V, false, 4, false, false> ARGS; \
     if (v.gstate) return v.uni ? FN<V, false, 1, false, true> ARGS : FN<V, false, 1, false, false> ARGS; \
     if (v.nobase) return v.uni ? FN<V, false, 3, false, true> ARGS : FN<V, false, 3, false, false> ARGS; \
     return v.uni ? FN<V, false, 0, false, true> ARGS : FN<V, false, 0, false, false> ARGS;
