@@ -371,10 +371,16 @@ def main():
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_s = float(total_ms.item()) / 1e3
     value = cfg.neighbours * K / total_s
-    # per round: the divergence-order kernel and the 6 kernels of its radix sort (CUB, compiled into
-    # our library), the evaluator's main pass and its two overflow passes; per improvement:
-    # apply_move, the base re-recording and its checkpoint shift (profiles/r01_launches.csv)
-    launches = 10 * K + 3 * improved
+    # per round: the divergence-order kernel and its radix sort (CUB, compiled into our library:
+    # histogram, exclusive sum, one onesweep pass per 8 key bits — the keys need the bits of 3Pm),
+    # the evaluator's main pass and its two overflow passes; per improvement: apply_move, the base
+    # re-recording and its checkpoint shift (profiles/r02_launches.csv)
+    span = inst.num_stages * 3 * inst.num_microbatches
+    key_bits = 1
+    while key_bits < 32 and span >> key_bits:
+        key_bits += 1
+    per_round = 1 + 2 + (key_bits + 7) // 8 + 3
+    launches = per_round * K + 3 * improved
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": 1000 * total_s / K, "higher_is_better": True,
