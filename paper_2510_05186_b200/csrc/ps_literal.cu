@@ -81,8 +81,18 @@ __device__ void ledger_add(Pt *pts, int *n, int64_t t, int64_t d) {
     ++*n;
 }
 
+// The candidates this pass replays (flagged malformed or out of range), compacted by one thread
+// per candidate: the replay threads then walk only those (usually none).
+__global__ void collect_kernel(const uint32_t *flags, int64_t N, int32_t *list) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    const uint32_t f = flags[c];
+    if (f == FLAG_MALFORMED || f == FLAG_RANGE) list[1 + atomicAdd(list, 1)] = (int32_t)c;
+}
+
 template <typename V>
-__global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_words, int slots) {
+__global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_words, int slots,
+                               const int32_t *list) {
     const int P = p.P, m = p.m, G = p.G, L = p.L;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= slots) return;
@@ -110,7 +120,9 @@ __global__ void literal_kernel(const EvalParams p, int64_t *scratch, int slot_wo
     int32_t *pend = rc_n + (size_t)P * m;          // [P*m] (derived mode) requested, not yet reloaded
     uint8_t *req = reinterpret_cast<uint8_t *>(pend + (size_t)P * m);   // [P*m] bit0 offload, bit1 reload requested
     const int mwords = (P * m + 31) / 32;
-    for (int64_t c = tid; c < p.N; c += slots) {
+    const int n_list = *list;
+    for (int k = tid; k < n_list; k += slots) {
+        const int64_t c = list[1 + k];
         const uint32_t flag_in = p.flags[c];
         if (flag_in != FLAG_MALFORMED && flag_in != FLAG_RANGE) continue;
         // ---- op codes and offload bits must name ops of the instance --------------------------
@@ -351,10 +363,18 @@ size_t literal_slot_bytes(int P, int m, int G) {
 
 cudaError_t literal_launch(const EvalParams &p, bool v64, int64_t *scratch, int slots, cudaStream_t s) {
     const int slot_words = (int)(literal_slot_bytes(p.P, p.m, p.G) / 8);
+    int32_t *list = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&list, (size_t)(p.N + 1) * sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(list, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    collect_kernel<<<(unsigned)((p.N + 255) / 256), 256, 0, s>>>(p.flags, p.N, list);
     const int block = 64, grid = (slots + block - 1) / block;
-    if (v64) literal_kernel<long long><<<grid, block, 0, s>>>(p, scratch, slot_words, slots);
-    else literal_kernel<int><<<grid, block, 0, s>>>(p, scratch, slot_words, slots);
-    return cudaGetLastError();
+    if (v64) literal_kernel<long long><<<grid, block, 0, s>>>(p, scratch, slot_words, slots, list);
+    else literal_kernel<int><<<grid, block, 0, s>>>(p, scratch, slot_words, slots, list);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaFreeAsync(list, s);
 }
 
 }  // namespace ps
