@@ -1122,17 +1122,15 @@ static int eval_batch_impl(const ps_instance *I, const ps_cand_batch *b, const p
 __global__ void delta_rows_kernel(int64_t N, int P, int stride, int mask_words, const uint16_t *ref,
                                   const uint32_t *ref_mask, uint16_t *out, uint32_t *out_mask,
                                   const unsigned long long *moves) {
-    const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // one warp per candidate (only the general ones are rebuilt; the rest are evaluated as moves)
+    const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (row >= N * P) return;
-    const int64_t c = row / P;
-    if (moves && unpack_move(moves[c]).type != MOVE_GENERAL) return;    // (evaluated as a move)
-    const int s = (int)(row % P);
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(ref + (size_t)s * stride);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(out + ((size_t)c * P + s) * stride);
-    for (int q = lane; q < stride / 2; q += 32) dst[q] = src[q];
-    if (s == 0)
-        for (int w = lane; w < mask_words; w += 32) out_mask[(size_t)c * mask_words + w] = ref_mask[w];
+    if (c >= N) return;
+    if (moves && unpack_move(moves[c]).type != MOVE_GENERAL) return;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(ref);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(out + (size_t)c * P * stride);
+    for (int q = lane; q < P * stride / 2; q += 32) dst[q] = src[q];
+    for (int w = lane; w < mask_words; w += 32) out_mask[(size_t)c * mask_words + w] = ref_mask[w];
 }
 
 // One thread per candidate: apply its differences (after delta_rows_kernel, same stream).
@@ -1327,7 +1325,7 @@ int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, cons
         // pass 2: the general candidates, rebuilt in HBM and evaluated materialised
         uint16_t *ord = (uint16_t *)(arena + off[A_ORD]);
         uint32_t *msk = (uint32_t *)(arena + off[A_MASK]);
-        const int64_t warps = N * I->P;
+        const int64_t warps = N;
         delta_rows_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(
             N, I->P, I->stride, I->mask_words, ref_d, rmask_d, ord, msk, moves);
         delta_apply_kernel<<<(unsigned)((N + 127) / 128), 128, 0, s>>>(
