@@ -129,13 +129,15 @@ def _row_codes(m: int, fill: int) -> "np.ndarray":
     return np.asarray(codes, np.uint16)
 
 
-def generate_all(inst: PipelineInstance, params: AdaParams = AdaParams(), device=None) -> dict:
+def generate_all(inst: PipelineInstance, params: AdaParams = AdaParams(), device=None, types=None,
+                 spans: dict | None = None) -> dict:
     """Every generator's schedule (or InfeasibleSchedule) from one batched evaluation.
 
     The whole AdaOffload back-off sequence (738 structures at 32 x 256) is encoded from one row per
     fill value (filled_order does not depend on the stage) and evaluated in one launch without
     traces; only the structures that become answers — AdaOffload's first feasible entry and the
-    other three generators — are re-run with their traces and decoded into Schedules."""
+    other three generators — are re-run with their traces and decoded into Schedules (of the
+    reference's own types with ``types=``; ``spans`` receives each answer's makespan)."""
     import numpy as np
     import torch
     from .engine import device_instance
@@ -185,7 +187,10 @@ def generate_all(inst: PipelineInstance, params: AdaParams = AdaParams(), device
             structs[name] = ({i: filled_order(inst, i, f[i]) for i in range(1, P + 1)},
                              frozenset() if name == "1f1b" else everything)
     names = list(structs)
-    decoded = dict(zip(names, run_orders(inst, [structs[k] for k in names], device=device)))
+    decoded = dict(zip(names, run_orders(inst, [structs[k] for k in names], device=device, types=types)))
+    if spans is not None:
+        makespans = res.makespan.cpu().numpy()
+        spans.update({name: int(makespans[c]) for name, c in picks.items() if c is not None and flags[c] & 1})
     seq_ok = all(inst.mem_delta[OpId(i, j, F)] <= inst.mem_limit[i]
                  for i in range(1, P + 1) for j in range(1, m + 1))
     out = {}

@@ -50,6 +50,61 @@ def gpu_run_order_for(ref_pkg):
     return run_order
 
 
+_GENERATORS = ("ada_offload", "pipeoffload_like", "one_f_one_b", "sequential_schedule", "best_feasible")
+_GEN_SITES = ("heuristics", "cache", "online")
+
+
+def gpu_generators_for(ref_pkg, originals: dict):
+    """The reference's generators (heuristics.py:50-210) with the whole AdaOffload back-off
+    sequence and the other three structures timed in one batched launch (heuristics.generate_all),
+    answers decoded into the reference's own Schedule type.  A generator whose structure is
+    infeasible defers to the reference's own function (through the GPU run_order), which raises
+    its own InfeasibleSchedule with its own message."""
+    from . import heuristics as _heur
+    ref_h = importlib.import_module(ref_pkg.__name__ + ".heuristics")
+    ref_sched = importlib.import_module(ref_pkg.__name__ + ".schedule")
+    names = {"ada_offload": "ada", "pipeoffload_like": "pipeoffload", "one_f_one_b": "1f1b",
+             "sequential_schedule": "sequential"}
+
+    def _all(inst, params):
+        spans: dict = {}
+        out = _heur.generate_all(inst, _heur.AdaParams(tolerance=params.tolerance), types=ref_sched, spans=spans)
+        return out, spans
+
+    def single(fn_name, takes_params):
+        key = names[fn_name]
+
+        def gen(inst, params=ref_h.AdaParams()):
+            out, _ = _all(inst, params)
+            if isinstance(out[key], Exception):
+                return originals[fn_name](inst, params) if takes_params else originals[fn_name](inst)
+            return out[key]
+        if not takes_params:
+            def gen_noparams(inst):
+                return gen(inst)
+            gen_noparams.__doc__ = f"GPU-batched drop-in for pipesched.heuristics.{fn_name}."
+            return gen_noparams
+        gen.__doc__ = f"GPU-batched drop-in for pipesched.heuristics.{fn_name}."
+        return gen
+
+    def best_feasible(inst, params=ref_h.AdaParams()):
+        out, spans = _all(inst, params)
+        best = None
+        for key in ("ada", "pipeoffload", "1f1b", "sequential"):        # _GENERATORS order, first wins ties
+            if isinstance(out[key], Exception):
+                continue
+            if best is None or spans[key] < best[0]:
+                best = (spans[key], out[key], key)
+        if best is None:
+            raise ref_h.NoFeasibleSchedule("all generators failed on this instance")
+        return best[1], best[2]
+
+    best_feasible.__doc__ = "GPU-batched drop-in for pipesched.heuristics.best_feasible (heuristics.py:196)."
+    return {"ada_offload": single("ada_offload", True), "pipeoffload_like": single("pipeoffload_like", False),
+            "one_f_one_b": single("one_f_one_b", False), "sequential_schedule": single("sequential_schedule", False),
+            "best_feasible": best_feasible}
+
+
 @dataclass(frozen=True)
 class WarmSearch:
     """How the GPU local search improves a warm start before the reference solver sees it."""
@@ -135,10 +190,11 @@ def search_fed_start_session(ref_pkg, search: WarmSearch = WarmSearch()):
     return start_session
 
 
-def install(ref_pkg, search: WarmSearch | None = None) -> None:
-    """Point the reference's run_order call sites at the GPU evaluator; with ``search``, also
-    let its ``start_session`` (and so ``solve`` and ``online_sim``) start from the GPU local
-    search's winner."""
+def install(ref_pkg, search: WarmSearch | None = None, generators: bool = True) -> None:
+    """Point the reference's run_order call sites at the GPU evaluator; with ``generators``, also
+    its generators and ``best_feasible`` at the batched GPU versions (one launch for the whole
+    AdaOffload back-off sequence); with ``search``, also let its ``start_session`` (and so
+    ``solve`` and ``online_sim``) start from the GPU local search's winner."""
     fn = gpu_run_order_for(ref_pkg)
     for site in _SITES:
         mod = importlib.import_module(f"{ref_pkg.__name__}.{site}")
@@ -146,6 +202,17 @@ def install(ref_pkg, search: WarmSearch | None = None) -> None:
             _saved.setdefault((ref_pkg.__name__, site), mod.run_order)
             mod.run_order = fn
     ref_pkg.run_order = fn
+    if generators:
+        ref_h = importlib.import_module(ref_pkg.__name__ + ".heuristics")
+        originals = {name: _saved.get((ref_pkg.__name__, f"heuristics.{name}"), getattr(ref_h, name))
+                     for name in _GENERATORS}
+        gens = gpu_generators_for(ref_pkg, originals)
+        for site in _GEN_SITES + ("",):
+            mod = importlib.import_module(f"{ref_pkg.__name__}.{site}") if site else ref_pkg
+            for name in _GENERATORS:
+                if hasattr(mod, name):
+                    _saved.setdefault((ref_pkg.__name__, f"{site or 'pkg'}.{name}"), getattr(mod, name))
+                    setattr(mod, name, gens[name])
     if search is not None:
         ref_solver = importlib.import_module(ref_pkg.__name__ + ".solver")
         ref_online = importlib.import_module(ref_pkg.__name__ + ".online")
@@ -158,6 +225,12 @@ def install(ref_pkg, search: WarmSearch | None = None) -> None:
 
 
 def uninstall(ref_pkg) -> None:
+    for site in _GEN_SITES + ("",):
+        mod = importlib.import_module(f"{ref_pkg.__name__}.{site}") if site else ref_pkg
+        for name in _GENERATORS:
+            key = (ref_pkg.__name__, f"{site or 'pkg'}.{name}")
+            if key in _saved:
+                setattr(mod, name, _saved.pop(key))
     for site in _SITES:
         key = (ref_pkg.__name__, site)
         if key in _saved:

@@ -15,16 +15,25 @@ def test_install_points_every_reference_call_site_at_the_gpu_path():
         import pipesched
         from pipesched import cache, heuristics, listsched
         from paper_2510_05186_b200 import integrate
+        from pipesched import online
         cpu = listsched.run_order
+        cpu_best = heuristics.best_feasible
+        cpu_ada = heuristics.ada_offload
         integrate.install(pipesched)
         try:
             for mod in (listsched, heuristics, cache, pipesched):
                 assert mod.run_order is not cpu
                 assert "GPU" in mod.run_order.__doc__
+            for mod in (heuristics, cache, online, pipesched):
+                assert mod.best_feasible is not cpu_best and "GPU-batched" in mod.best_feasible.__doc__
+            assert heuristics.ada_offload is not cpu_ada and pipesched.ada_offload is heuristics.ada_offload
         finally:
             integrate.uninstall(pipesched)
         for mod in (listsched, heuristics, cache, pipesched):
             assert mod.run_order is cpu
+        for mod in (heuristics, cache, online, pipesched):
+            assert mod.best_feasible is cpu_best
+        assert heuristics.ada_offload is cpu_ada and pipesched.ada_offload is cpu_ada
     finally:
         sys.path.remove(REF)
 
