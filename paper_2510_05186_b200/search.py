@@ -37,7 +37,8 @@ class SearchConfig:
     max_shift: int = 4
     share_prefix: bool = True        # resume neighbours from checkpoints of the incumbent
     dedup: bool = True               # simulate a move drawn several times in a round once
-    prune: bool = True               # abandon neighbours that provably cannot improve
+    prune: bool = False              # abandon neighbours that provably cannot improve (
+                                     # same trail, measured no faster: off by default)
     # Iterated local search: after `descent_patience` rounds without improving
     # the current point, restart the descent from the best structure kicked by `kick_moves`
     # random moves.  0 = plain descent (a run then ends at convergence or its budget).

@@ -563,6 +563,22 @@ def test_bound_pruning_keeps_every_round_decision(cuda_ok, late):
     assert adopted >= 1 or late
 
 
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_pruned_descent_follows_the_full_trail(cuda_ok, cfg):
+    """SearchConfig(prune=True) against the default: the whole descent to convergence adopts the
+    same moves (same improvement trail and final structure)."""
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    runs = []
+    for prune in (False, True):
+        ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=65536, prune=prune))
+        while ls.stale < 16 and ls.round < 3000:
+            ls.step()
+        o, m = ls.incumbent_structure()
+        runs.append(([(i.round, i.makespan, i.index) for i in ls.improvements], ls.round, o, m))
+    assert runs[0] == runs[1]
+    assert len(runs[0][0]) > 3
+
+
 @pytest.mark.parametrize("late", [False, True])
 def test_suffix_sharing_equals_full_simulation(cuda_ok, late):
     """Every neighbour of config-3 search rounds (65,536 each, from the warm start and from the late
