@@ -616,8 +616,7 @@ def main():
                "neighbours_per_round": cfg.neighbours,
                "ms_per_round_mean": sum(r_ms) / len(r_ms), "ms_per_round_last50": sum(r_ms[-50:]) / len(r_ms[-50:]),
                "note": "LocalSearch as shipped: a move drawn several times in a round is simulated once "
-                       "(lowest index) and a neighbour whose makespan bound reaches the incumbent's is "
-                       "abandoned (DESIGN.md 3.13); the trajectory is that of evaluating every neighbour"}
+                       "(lowest index; DESIGN.md 3.7); the trajectory is that of evaluating every neighbour"}
         if "cpu_baseline" in line:
             ttb["cpu_port_seconds_to_best_estimate"] = ttb["rounds_to_best"] * cfg.neighbours / line["cpu_baseline"]["value"]
             # the same search on the CPU with the same deduplication of repeated moves
