@@ -151,7 +151,7 @@ struct Plan {
 int words_per_candidate(const ps_instance *I, int K, int order_bytes = 0) {
     int vw = I->v64 ? 2 : 1;
     int nz = 2 * I->P * I->m + 3 * I->P * I->MW;
-    int w = I->P * 2 * K * (vw + 1) + ((nz + 1) & ~1) + I->P * I->stride * order_bytes / 4;
+    int w = I->P * 2 * K * (vw + 1) + ((nz + 3) & ~3) + I->P * I->stride * order_bytes / 4;   // rows 16-byte aligned
     return (w + 3) & ~3;
 }
 

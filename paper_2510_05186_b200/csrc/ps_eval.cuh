@@ -355,8 +355,9 @@ eval_kernel(const EvalParams p) {
                                      : gsw;
 #define SWW(off) (GSTATE ? wsw[(off)] : smem[sbase + (off)])
 #define SVW(off) (GSTATE ? reinterpret_cast<V *>(wsw)[(off)] : reinterpret_cast<V *>(smem)[sbase / VW + (off)])
-    // materialised candidates: the candidate's stage orders, staged once (8-byte aligned)
-    const int o_row = o_A + ((nz + 1) & ~1);
+    // materialised candidates: the candidate's stage orders, staged once (16-byte aligned: row8
+    // reads eight uint16 codes at a time; the state start and o_A are 16-byte aligned)
+    const int o_row = o_A + ((nz + 3) & ~3);
     const int row_bytes = P * p.stride * (p.order_u8 ? 1 : 2);
 
     const int chan_i = has_stage ? __ldg(&p.chan[i]) : -1;
