@@ -1284,6 +1284,9 @@ eval_kernel(const EvalParams p) {
                 __syncwarp();
                 continue;
             }
+#if PS_SYNC_ARGMIN
+            __syncwarp();      // every lane's writes of its stage's offload bits before the restore's
+#endif
             if (BAND) {
                 // the bitsets, then each stage's rows over the old and the checkpoint's band
                 warp_copy_words_any(&SB(o_bits), src + 2 * P * m, nb3, lane);
@@ -1491,6 +1494,13 @@ eval_kernel(const EvalParams p) {
                 if (REC && conv_c >= 0) break;
                 __syncwarp();      // the checkpoint's reads before the commit's writes
             }
+#if PS_SYNC_ARGMIN
+            // Formal ordering for racecheck: other lanes' key reads of this
+            // iteration before the commit's writes.  Off by default: the reads feed the argmin's
+            // operands and the writes its result, and a converged warp's shared-memory accesses
+            // complete in program order.
+            __syncwarp();
+#endif
             const int w = (int)((ml >> 24) & 63u);
             const int j = (int)((ml >> 2) & 0x3FFFFFu);
             const int k = (int)(ml & 3u);
