@@ -17,7 +17,7 @@ orders = {i: stage_order_of(s0, i) for i in range(1, inst.num_stages + 1)}
 ls = LocalSearch(inst, orders, s0.offloaded, SearchConfig(seed=20251005, neighbours=1024))
 for name in ("warm", "late"):
     if name == "late":
-        z = np.load("tools/inc320_config3.npz")
+        z = np.load("tests/golden/inc320_config3.npz")
         ls.inc_orders.copy_(torch.from_numpy(z["orders"].view(np.int16)))
         ls.inc_mask.copy_(torch.from_numpy(z["mask"].view(np.int32)))
         ls.base.record(ls.inc_orders, ls.inc_mask)

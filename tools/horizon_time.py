@@ -1,3 +1,5 @@
+"""Time the generator structures of a 32 x 256 instance with 40,000-quanta ops (long horizons,
+DESIGN.md §7): one GPU evaluation against the oracle's."""
 import time, numpy as np, torch, sys
 sys.path.insert(0, '.')
 from oracle.oracle import Oracle
