@@ -217,3 +217,37 @@ def test_batch_paths_on_random_instances_match_the_oracle(cuda_ok, seed):
     if r is None:
         pytest.skip("no feasible warm start drawn")
     assert r[2] == 2048 * 3
+
+
+def soak_ils_case(seed: int, stages=(2, 10), microbatches=(4, 24), n=512, kicks=3, kick_moves=4, big=False):
+    """Iterated local search (descents, kicks from the best) on one random instance
+    against the CPU restatement (tests/_search_cpu.py): the same improvement trail, round and kick
+    counts and best structure."""
+    from _search_cpu import cpu_search
+    from oracle.oracle import Oracle
+    from paper_2510_05186_b200.listsched import stage_order_of
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+    start = _random_start(seed, stages, microbatches, big)
+    if start is None:
+        return None
+    inst, s0 = start
+    P = inst.num_stages
+    cfg = SearchConfig(seed=seed, neighbours=n, shift_permille=600, max_shift=6, kick_moves=kick_moves)
+    ls = LocalSearch(inst, {i: stage_order_of(s0, i) for i in range(1, P + 1)}, s0.offloaded, cfg)
+    want = cpu_search(Oracle(ls.di.packed), ls.inc_orders.cpu().numpy().view(np.uint16),
+                      ls.inc_mask.cpu().numpy().view(np.uint32), cfg.seed, cfg.shift_permille, cfg.max_shift, n,
+                      kick_moves=kick_moves, kicks=kicks)
+    res = ls.run(kicks=kicks)
+    assert [(i.round, i.makespan, i.index) for i in res.improvements] == want["trail"], seed
+    assert (ls.round, ls.kicks) == (want["rounds"], want["kicks"]), seed
+    assert res.makespan == want["best_span"]
+    assert (ls.best_orders.cpu().numpy().view(np.uint16) == want["best_orders"]).all()
+    assert (ls.best_mask.cpu().numpy().view(np.uint32) == want["best_mask"]).all()
+    return P, inst.num_microbatches, ls.round * n
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_iterated_local_search_on_random_instances_follows_the_cpu_restatement(cuda_ok, seed):
+    r = soak_ils_case(400 + seed, big=seed % 3 == 2)
+    if r is None:
+        pytest.skip("no feasible warm start drawn")
