@@ -11,7 +11,7 @@ from paper_2510_05186_b200.instance import OpId, OpKind, instance_from_dict
 from paper_2510_05186_b200.packing import PAD_CHANNEL, pack_instance
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
-CORPORA = ("ref_tests", "fuzz", "configs")
+CORPORA = ("ref_tests", "fuzz", "configs", "random")
 MALFORMED = "malformed"
 
 
