@@ -271,8 +271,12 @@ int plan_pass(const ps_instance *I, bool moves, int K, int64_t N, Plan *pl, int 
         // the incumbent (48 KB at config 5), so 1-warp blocks left only 4 warps per SM resident.
         pl->gstate = true;
         pl->warps = moves ? std::max(1, std::min(PS_GSTATE_MAX_WARPS, env_int("PS_GSTATE_WARPS", PS_GSTATE_MAX_WARPS))) : 1;
-        // behind it, each warp's offload / pending-transfer bitsets (read on most events)
-        pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * ((3 * I->P * I->MW + 3) & ~3)) * 4;
+        // behind it, each warp's offload / pending-transfer bitsets (read on most events); fewer
+        // warps per block when a large incumbent leaves no room for all of theirs (P = 32, m = 1024)
+        const int bits_w = (3 * I->P * I->MW + 3) & ~3;
+        while (pl->warps > 1 && (size_t)(pl->inc_words + pl->warps * bits_w) * 4 > (size_t)I->max_smem_optin)
+            pl->warps = (pl->warps + 1) / 2;
+        pl->cfg.smem = (size_t)(pl->inc_words + pl->warps * bits_w) * 4;
         // and, when they fit, their ledger windows (the event loop's other hot words)
         const size_t win = (size_t)pl->warps * I->P * 2 * pl->K * ((I->v64 ? 2 : 1) + 1) * 4;
         pl->win_smem = env_int("PS_WIN_SMEM", 1) != 0 &&
@@ -1484,6 +1488,57 @@ int ps_bound_batch_eval(const ps_instance *I, const ps_bound_batch *b, int64_t *
     return PS_OK;
 }
 
+// The move-encoded kernels keep the incumbent in shared memory, with one warp's bitsets behind it.
+bool moves_incumbent_fits(const ps_instance *I) {
+    return (size_t)(incumbent_words(I, true) + ((3 * I->P * I->MW + 3) & ~3)) * 4 <= (size_t)I->max_smem_optin;
+}
+
+__global__ void best_key_kernel(const int64_t *span, const uint32_t *flags, int64_t n, int64_t first, long long *best);
+
+// A search round for an incumbent too large for shared memory (P = 32 with m above ~1,100): the
+// neighbours are materialised in chunks and evaluated as rows (with prefix sharing against the
+// recorded base), each chunk's best key folded into *best_key — the same key as the move-encoded
+// round (a duplicate move only costs its own evaluation).
+int search_round_rows(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
+                      cudaStream_t s) {
+    const size_t per = (size_t)I->P * I->stride * 2 + (size_t)I->mask_words * 4 + 8 + 8 + 4;
+    const int64_t cap = std::max<int64_t>(256, (int64_t)(((size_t)env_int("PS_ROWS_CHUNK_MB", 2048) << 20) / per));
+    const int64_t chunk = std::min<int64_t>(d->count, std::min<int64_t>(cap, 16384));
+    char *arena = nullptr;
+    PS_CUDA(cudaMallocAsync((void **)&arena, (size_t)chunk * per + 5 * 256, s));
+    size_t off = 0;
+    auto take = [&](size_t n) { char *q = arena + off; off += (n + 255) & ~(size_t)255; return q; };
+    uint16_t *ord = (uint16_t *)take((size_t)chunk * I->P * I->stride * 2);
+    uint32_t *msk = (uint32_t *)take((size_t)chunk * I->mask_words * 4);
+    int64_t *span = (int64_t *)take((size_t)chunk * 8);
+    double *bub = (double *)take((size_t)chunk * 8);
+    uint32_t *flg = (uint32_t *)take((size_t)chunk * 4);
+    int rc = PS_OK;
+    for (int64_t lo = 0; lo < d->count && rc == PS_OK; lo += chunk) {
+        const int64_t n = std::min(chunk, d->count - lo);
+        materialize_kernel<<<(unsigned)((n * I->P * 32 + 255) / 256), 256, 0, s>>>(
+            move_ctx(I), d->moves, d->round, d->first_index + lo, n, d->inc_orders, d->inc_mask, ord, msk);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { rc = cuda_fail(e, "materialize"); break; }
+        EvalParams p;
+        memset(&p, 0, sizeof p);
+        fill_instance(I, &p);
+        p.N = n;
+        p.orders = ord;
+        p.masks = msk;
+        p.makespan = makespan_out ? makespan_out + lo : span;
+        p.bubble = bub;
+        p.flags = flg;
+        p.events_total = (unsigned long long *)d->events_total;
+        if ((rc = run_eval(I, p, false, s, d->base)) != PS_OK) break;
+        best_key_kernel<<<std::max(1, std::min((int)((n + 255) / 256), 4 * I->num_sms)), 256, 0, s>>>(
+            p.makespan, flg, n, d->first_index + lo, (long long *)best_key);
+        if ((e = cudaGetLastError()) != cudaSuccess) rc = cuda_fail(e, "best key");
+    }
+    cudaFreeAsync(arena, s);
+    return rc;
+}
+
 int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best_key, int64_t *makespan_out,
                     void *stream) {
     NvtxRange nvtx("ps_search_round r=%llu", (unsigned long long)(d ? d->round : 0));
@@ -1513,6 +1568,10 @@ int ps_search_round(const ps_instance *I, const ps_search_desc *d, int64_t *best
     // (bound pruning sums a stage's remaining work in 32 bits: only where the horizon fits them)
     p.cutoff = makespan_out == nullptr && d->cutoff > 0 && I->time_safe == INT_MAX ? d->cutoff : 0;
     p.events_total = (unsigned long long *)d->events_total;
+    if (!moves_incumbent_fits(I) || env_int("PS_SEARCH_ROWS", 0) != 0) {     // (the knob: tests)
+        if (d->count == 0) return PS_OK;
+        return search_round_rows(I, d, best_key, makespan_out, (cudaStream_t)stream);
+    }
     return run_eval(I, p, true, (cudaStream_t)stream, d->base);
 }
 

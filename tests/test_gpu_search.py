@@ -615,3 +615,29 @@ def test_suffix_sharing_equals_full_simulation(cuda_ok, late):
     # peaks and bubbles: materialised neighbours with and without the base
     o, mk = ls.materialize(0, 4096, 0)
     _eval_both(ls.di, o, mk, ls.base)
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_materialised_search_rounds_equal_the_move_encoded_ones(cuda_ok, cfg, monkeypatch):
+    """An incumbent too large for shared memory (P = 32, m above ~1,100) is searched by
+    materialising the neighbours in chunks (search_round_rows in ps_abi.cu); forced here with
+    PS_SEARCH_ROWS=1 on configs 2/3: every neighbour's makespan of a round, and a whole descent's
+    trail and final structure, equal the move-encoded search's."""
+    import torch
+    inst, orders, off, LocalSearch, SearchConfig = _setup(cfg)
+    n = 4096
+    runs = []
+    for rows in ("0", "1"):
+        monkeypatch.setenv("PS_SEARCH_ROWS", rows)
+        ls = LocalSearch(inst, orders, off, SearchConfig(seed=SEED, neighbours=n))
+        ms = torch.empty(n, dtype=torch.int64, device="cuda")
+        ls.launch_round(ms)
+        torch.cuda.synchronize()
+        first = ms.cpu().numpy().copy()
+        ls.finish_round()
+        while ls.stale < 8 and ls.round < 60:
+            ls.step()
+        o, mk = ls.incumbent_structure()
+        runs.append((first, [(i.round, i.makespan, i.index) for i in ls.improvements], ls.round, o, mk))
+    assert (runs[0][0] == runs[1][0]).all()
+    assert runs[0][1:] == runs[1][1:] and len(runs[0][1]) > 3

@@ -4,7 +4,7 @@
 O=gpurun_out
 for knobs in "PS_FORCE_GSTATE=1" "PS_FORCE_GSTATE=1 PS_WIN_SMEM=0" "PS_WINDOW=4" "PS_CHECKPOINT_INTERVAL=1" \
              "PS_CHECKPOINT_INTERVAL=32" "PS_WMASK=0 PS_FORCE_GSTATE=1" "PS_NOBASE_BUILD=0" "PS_DYNAMIC=0 PS_ORDER=0" \
-             "PS_FORCE_GSTATE=1 PS_GSTATE_WARPS=1"; do
+             "PS_FORCE_GSTATE=1 PS_GSTATE_WARPS=1" "PS_SEARCH_ROWS=1"; do
   tag=$(echo $knobs | tr ' =' '_-')
   for path in "search 5000 30" "channel 5100 20" "batch 5200 20"; do
     set -- $path
