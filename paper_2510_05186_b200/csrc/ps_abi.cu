@@ -1240,6 +1240,8 @@ static bool valid_structure(const ps_instance *I, const uint16_t *ref) {
     return true;
 }
 
+bool moves_incumbent_fits(const ps_instance *I);
+
 int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, const ps_result_batch *r, void *stream) {
     NvtxRange nvtx("ps_eval_batch_host_delta n=%llu", (unsigned long long)(b ? b->num_candidates : 0));
     if (!I || !b || !r) return fail(PS_ERR_INVALID, "null argument");
@@ -1258,8 +1260,7 @@ int ps_eval_batch_host_delta(const ps_instance *I, const ps_delta_batch *b, cons
     // rounds do), when the reference is well formed, its incumbent copy fits in shared memory and no
     // time can leave the evaluator's range (PS_FLAG_RANGE candidates need rows for the 64-bit pass).
     const bool moves_ok = env_int("PS_DELTA_MOVES", 1) != 0 && I->time_safe == INT_MAX &&
-                          (size_t)incumbent_words(I, true) * 4 <= (size_t)I->max_smem_optin &&
-                          valid_structure(I, b->ref_orders);
+                          moves_incumbent_fits(I) && valid_structure(I, b->ref_orders);
     // device arena: the encoded batch, the move list, the general list and flags, the rebuilt
     // candidates, the outputs
     const size_t n_ref = (size_t)I->P * I->stride * 2, n_rmask = (size_t)I->mask_words * 4;

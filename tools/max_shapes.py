@@ -18,7 +18,7 @@ from oracle.oracle import Oracle  # noqa: E402
 from paper_2510_05186_b200 import make_uniform_instance  # noqa: E402
 from paper_2510_05186_b200.engine import DeviceInstance  # noqa: E402
 from paper_2510_05186_b200.heuristics import generator_structures  # noqa: E402
-from paper_2510_05186_b200.packing import encode_candidate, pack_instance  # noqa: E402
+from paper_2510_05186_b200.packing import delta_encode, encode_candidate, pack_instance  # noqa: E402
 from paper_2510_05186_b200.search import LocalSearch, SearchConfig  # noqa: E402
 
 
@@ -56,7 +56,7 @@ def run(P, m, n, rounds):
         out["search_setup_seconds"] = round(time.time() - t1, 2)
         t_gpu_rounds = t_cpu_rounds = 0.0
         ms = torch.empty(n, dtype=torch.int64, device="cuda")
-        checked, bad = 0, 0
+        checked, bad, bad_delta = 0, 0, 0
         for _ in range(rounds):
             inc_o = ls.inc_orders.cpu().numpy().view(np.uint16).copy()
             inc_m = ls.inc_mask.cpu().numpy().view(np.uint32).copy()
@@ -68,13 +68,18 @@ def run(P, m, n, rounds):
             best, want_ms = orc.search_round(inc_o, inc_m, 5, 700, 4, ls.round, 0, n, want_makespans=True)
             t_cpu_rounds += time.time() - t1
             bad += int((ms.cpu().numpy() != want_ms).sum())
+            # the same neighbours as a delta-encoded host batch (moves or rebuilt rows)
+            mo, mm = ls.materialize(0, n, ls.round)
+            d = delta_encode(inc_o, inc_m, mo.cpu().numpy().view(np.uint16), mm.cpu().numpy().view(np.uint32))
+            r = ls.di.evaluate_host_delta(inc_o, inc_m, *d, peak=False, base=ls.base)
+            bad_delta += int((np.asarray(r.makespan) != want_ms).sum())
             checked += n
             assert int(ls.best_key.item()) == best
             t1 = time.time()
             ls.finish_round()
             torch.cuda.synchronize()
             out["finish_seconds"] = round(out.get("finish_seconds", 0) + time.time() - t1, 2)
-        out.update({"gpu_round_seconds": round(t_gpu_rounds, 2), "oracle_round_seconds": round(t_cpu_rounds, 2),"search_checked": checked, "search_mismatches": bad, "final_makespan": ls.makespan,
+        out.update({"gpu_round_seconds": round(t_gpu_rounds, 2), "oracle_round_seconds": round(t_cpu_rounds, 2),"search_checked": checked, "search_mismatches": bad, "delta_mismatches": bad_delta, "final_makespan": ls.makespan,
                     "initial_makespan": ls.initial_makespan})
     out["seconds"] = round(time.time() - t0, 1)
     return out
