@@ -327,3 +327,33 @@ def test_explicit_channel_entries_out_of_range_are_malformed(cuda_ok):
         torch.cuda.synchronize()
         assert (r0.flags.cpu().numpy() == flags[good]).all()
         assert (r0.makespan.cpu().numpy() == r.makespan.cpu().numpy()[good]).all()
+
+
+@pytest.mark.parametrize("m", [1024, 1280])
+def test_search_rounds_at_the_stage_limit(cuda_ok, m):
+    """P = 32 (PS_MAX_STAGES) with a long incumbent: at m = 1024 the move-encoded kernel runs with
+    one-warp blocks (the incumbent takes 196 KB of shared memory); at m = 1280 it no longer fits and
+    the round materialises its neighbours. Every neighbour's makespan, the round's
+    best key and the delta-encoded host batch of the same neighbours against the oracle."""
+    import torch
+    from oracle.oracle import Oracle
+    from paper_2510_05186_b200 import make_uniform_instance
+    from paper_2510_05186_b200.heuristics import generator_structures
+    from paper_2510_05186_b200.packing import delta_encode
+    from paper_2510_05186_b200.search import LocalSearch, SearchConfig
+    inst = make_uniform_instance(32, m, 3, 2, 2, 1, 4, 2, 6)
+    o, f = generator_structures(inst)[-1]
+    n = 16
+    ls = LocalSearch(inst, o, f, SearchConfig(seed=5, neighbours=n, shift_permille=700, max_shift=4))
+    inc_o = ls.inc_orders.cpu().numpy().view(np.uint16).copy()
+    inc_m = ls.inc_mask.cpu().numpy().view(np.uint32).copy()
+    ms = torch.empty(n, dtype=torch.int64, device="cuda")
+    ls.launch_round(ms)
+    torch.cuda.synchronize()
+    best, want = Oracle(ls.di.packed).search_round(inc_o, inc_m, 5, 700, 4, 0, 0, n, want_makespans=True)
+    assert (ms.cpu().numpy() == want).all()
+    assert int(ls.best_key.item()) == best
+    mo, mm = ls.materialize(0, n, 0)
+    d = delta_encode(inc_o, inc_m, mo.cpu().numpy().view(np.uint16), mm.cpu().numpy().view(np.uint32))
+    r = ls.di.evaluate_host_delta(inc_o, inc_m, *d, peak=False, base=ls.base)
+    assert (np.asarray(r.makespan) == want).all()
